@@ -1,0 +1,369 @@
+#!/usr/bin/env python
+"""Bench harness: mixed-precision SLDG split step on B200 (arXiv:1603.07008).
+
+Metric (BASELINE.json): GDoF/s per advection step and achieved HBM GB/s (% of roofline).
+Default workload = BASELINE configs[4] ("C5"): 4D (x1,x2,v1,v2) dimension-split step on a
+128^4 grid, k=3 per dim (81 coefficients/cell), mixed precision (c_0 fp64, rest fp32),
+Landau-type initial value (eps=0.01) and per-line Vlasov CFL fields.  One step
+= 4 sweeps (x1, x2, v1, v2); a sweep reads and writes every stored coefficient once.
+With --gpus N (torchrun) the v2 dim is block-sharded; the v2 sweep exchanges halo layers
+over NCCL (strong scaling: total grid fixed).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl sldg|reference]
+                  [--config c5|c4|c3|c2] [--precision mixed|fp64] [--k K]
+
+Prints ONE JSON line on rank 0.  --impl reference times the CPU oracle (plain C, one host
+core) on a bounded sample of the same workload (sampled lines of every sweep).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import sldg_inputs  # noqa: E402
+
+CONFIGS = {
+    # name: (dims, kinds, k, lo, hi, description)
+    "c5": ([128, 128, 128, 128], ["x", "x", "v", "v"], 3,
+           "4D split step 128^4, k=3 (BASELINE configs[4])"),
+    "c4": ([64, 64, 64, 64], ["x", "x", "v", "v"], 2, "4D split step 64^4, k=2 (BASELINE configs[3])"),
+    "c3": ([4096, 4096], ["x", "v"], 4, "2D 4096^2 split step (BASELINE configs[2])"),
+    "c2": ([1024, 1024], ["x", "v"], 4, "2D 1024^2 split step (BASELINE configs[1])"),
+}
+
+
+def domain(kinds):
+    lo = [0.0 if t == "x" else -6.0 for t in kinds]
+    hi = [4 * np.pi if t == "x" else 6.0 for t in kinds]
+    return lo, hi
+
+
+def bytes_per_cell(K: int, precision: str) -> int:
+    """One stored cell: fp64 c_0 + (K-1) fp32 (mixed) or K fp64."""
+    return 8 + 4 * (K - 1) if precision == "mixed" else 8 * K
+
+
+def memorydown(o: int, d: int) -> float:
+    """8o / (8d + 4(o-d)) (Tables III-VI 'memorydown')."""
+    return 8.0 * o / (8.0 * d + 4.0 * (o - d))
+
+
+def load_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------------
+# CPU oracle (cpu_baseline leg and --impl reference): sampled lines of every sweep
+# ---------------------------------------------------------------------------------------------
+def oracle_sample(dims, kinds, k, precision, lines_per_sweep: int, seed: int = 1603):
+    """Time the CPU oracle on `lines_per_sweep` random lines of each sweep of the split step.
+    Returns (seconds, dofs).  Inputs are the parity generator's values for those cells."""
+    import oracle  # test infrastructure; only this leg of bench.py may use it
+
+    D, K = len(dims), k ** len(dims)
+    nd = 1 if precision == "mixed" else K
+    lo, hi = domain(kinds)
+    rng = np.random.default_rng(seed)
+    S = np.cumprod([1] + list(dims[:-1]))
+    secs, dofs = 0.0, 0
+    for d, field, mask in sldg_inputs.vlasov_fields(dims, kinds, lo, hi):
+        fd = [e for e in range(D) if mask >> e & 1]
+        for _ in range(lines_per_sweep):
+            perp = {e: int(rng.integers(0, dims[e])) for e in range(D) if e != d}
+            base = sum(perp[e] * S[e] for e in perp)
+            cells = base + np.arange(dims[d]) * S[d]
+            src = oracle.round_layout(sldg_inputs.random_coeffs(dims, k, seed, cells=cells), K, nd)
+            fi, st = 0, 1
+            for e in fd:
+                fi += perp[e] * st
+                st *= dims[e]
+            ldims = [1] * D
+            ldims[d] = dims[d]
+            t0 = time.perf_counter()
+            oracle.advect(src, ldims, k, d, shift=float(field[fi]), n_double=nd)
+            secs += time.perf_counter() - t0
+            dofs += dims[d] * K
+    return secs, dofs
+
+
+def run_reference(args, dims, kinds, k, cfg_json):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    lines = args.ref_lines
+    for _ in range(args.warmup):
+        oracle_sample(dims, kinds, k, args.precision, max(1, lines // 8))
+    t_total, dof_total = 0.0, 0
+    for s in range(args.steps):
+        t, n = oracle_sample(dims, kinds, k, args.precision, lines, seed=1603 + s)
+        t_total += t
+        dof_total += n
+    value = dof_total / t_total / 1e9
+    bpd = bytes_per_cell(k ** len(dims), args.precision) / k ** len(dims)
+    sample = (f"{lines} random lines per sweep x {len(dims)} sweeps per step of the {args.config} workload "
+              f"(oracle.advect on each line, same k, same per-line CFL); timed oracle calls only")
+    out = {
+        "impl": "reference", "metric": "GDoF/s per advection sweep (split step of all dims)",
+        "value": value, "unit": "GDoF/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg_json,
+        "hbm_gbs_equiv": value * bpd * 2,
+        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return 0
+
+
+# ---------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="sldg", choices=["sldg", "reference"])
+    ap.add_argument("--config", default="c5", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="mixed", choices=["mixed", "fp64"])
+    ap.add_argument("--k", type=int, default=None)
+    ap.add_argument("--eps", type=float, default=0.01)
+    ap.add_argument("--ref-lines", type=int, default=2048)
+    ap.add_argument("--cpu-lines", type=int, default=12000)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweeps", default=None, help="comma list of dims to run (default: all)")
+    args = ap.parse_args()
+
+    dims, kinds, k0, desc = CONFIGS[args.config]
+    k = args.k or k0
+    D, K = len(dims), k ** len(dims)
+    cells = int(np.prod(dims))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    sweep_dims = list(range(D)) if args.sweeps is None else [int(x) for x in args.sweeps.split(",")]
+    cfg_json = {"workload": f"{args.config}: {desc}", "dims": dims, "k": k, "coeffs_per_cell": K,
+                "precision": args.precision, "ic": f"landau eps={args.eps}", "sweeps_per_step": len(sweep_dims),
+                "parallelism": f"shard v{D // 2 if D > 2 else 1} (dim {D - 1}) x{world}" if world > 1 else "1 GPU",
+                "l2": "inputs larger than L2 (no flush needed)" if cells * bytes_per_cell(K, args.precision) > 4 * 126e6
+                else "inputs comparable to L2 (126 MB): L2 residency possible",
+                "dt": 0.1}
+    if args.impl == "reference":
+        return run_reference(args, dims, kinds, k, cfg_json)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_1603_07008_b200 import Grid, sldg
+
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        uid = [sldg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        uid = uid[0]
+    else:
+        uid = None
+
+    lo, hi = domain(kinds)
+    g = Grid(dims, k, lo=lo, hi=hi, precision=args.precision, rank=rank, world=world, unique_id=uid,
+             max_halo=2)
+    terms = sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=args.eps)
+    g.fill_separable(terms)
+    sweeps = [s for s in sldg_inputs.vlasov_fields(dims, kinds, lo, hi, eps=args.eps) if s[0] in sweep_dims]
+    dev_fields = [torch.tensor(f, dtype=torch.float64, device="cuda") for _, f, _ in sweeps]
+    stream = torch.cuda.ExternalStream(g.stream())
+    torch.cuda.synchronize()
+
+    def step():
+        for (d, _, m), tf in zip(sweeps, dev_fields):
+            g.advect_device(d, tf.data_ptr(), m)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        g.sync()
+
+    mass0 = g.mass()
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    # ---------------------------------------------------------------- device-timed region
+    g.kernel_time(reset=True)
+    g.profile(True)
+    launches0 = g.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        barrier()
+    g.profile(False)
+    ms = e0.elapsed_time(e1)
+    launches = g.launch_count() - launches0
+    kt_all = g.kernel_time(-1)
+    per_dim = {d: g.kernel_time(d) for d in sweep_dims}
+    t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    mass1 = g.mass()
+
+    # ---------------------------------------------------------------- end-to-end (C ABI, host buffers)
+    e2e = None
+    if not args.no_e2e:
+        pinned = []
+        for _, f, _ in sweeps:
+            pt = torch.empty(len(f), dtype=torch.float64, pin_memory=True)
+            pt.numpy()[:] = f
+            pinned.append(pt)
+        h2d = sum(p.numel() * 8 for p in pinned)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for (d, _, m), p in zip(sweeps, pinned):
+                g.advect(d, field=p.numpy(), field_mask=m)
+            g.mass()  # D2H read of the step's diagnostic (blocking)
+        barrier()
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item())
+        e2e = {"value": len(sweeps) * cells * K * args.steps / e2e_s / 1e9, "unit": "GDoF/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * world,
+               "api": "sldg_advect (host pinned CFL fields, one per sweep) + sldg_mass (D2H) per step"}
+
+    if rank == 0:
+        peak, peak_src = load_peak()
+        step_ms = ms_max / args.steps
+        dofs_per_step = len(sweeps) * cells * K
+        alg_bytes_step = len(sweeps) * 2 * cells * bytes_per_cell(K, args.precision)
+        value = dofs_per_step / (step_ms * 1e-3) / 1e9
+        # dominant kernel = the sweep dim with the largest total kernel time (rank-0 view)
+        dom = max(per_dim, key=lambda d: per_dim[d][0])
+        d_ms, d_n, d_bytes = per_dim[dom]
+        achieved = (d_bytes / d_n) / (d_ms / d_n * 1e-3) / 1e9 if d_n else None
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_dram.json")) as f:
+                nd = json.load(f)
+            key = f"{args.config}_{args.precision}_k{k}_dim{dom}"
+            traffic = nd.get(key)
+        except Exception:
+            pass
+        cpu = None
+        if not args.no_cpu_baseline and world == 1:
+            secs, dofs = oracle_sample(dims, kinds, k, args.precision, args.cpu_lines)
+            cpu = {"value": dofs / secs / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "oracle",
+                   "sample": f"{args.cpu_lines} random lines per sweep x {len(sweeps)} sweeps of the same "
+                             f"workload ({dofs} DoF, {secs:.1f} s of oracle time)"}
+        out = {
+            "metric": "GDoF/s per advection sweep (split step of all dims)",
+            "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64 arithmetic; storage " + ("c0 fp64 + fp32" if args.precision == "mixed" else "fp64"),
+            "data": "synthetic (Landau-type IC, Vlasov CFL fields)", "config": cfg_json,
+            "hbm_gbs": alg_bytes_step / (step_ms * 1e-3) / 1e9 / world,
+            "hbm_frac_of_peak": alg_bytes_step / (step_ms * 1e-3) / 1e9 / world / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "kernel": f"sweep along dim {dom} ({'sweep_d0_kernel' if dom == 0 else 'sweep_strided_kernel'})",
+                         "peak_source": peak_src,
+                         "bytes_per_launch": d_bytes / d_n if d_n else None,
+                         "avg_launch_ms": d_ms / d_n if d_n else None},
+            "sweeps": {str(d): {"ms_per_launch": per_dim[d][0] / max(1, per_dim[d][1]),
+                                "gbs": (per_dim[d][2] / (per_dim[d][0] * 1e-3) / 1e9) if per_dim[d][0] else None}
+                       for d in per_dim},
+            "kernel_share_of_step": kt_all[0] / ms if ms else None,
+            "gpu_launches": launches,
+            "mass_rel_drift": abs(mass1 - mass0) / abs(mass0),
+            "clocks": clk.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(out))
+    g.destroy()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

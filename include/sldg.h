@@ -1,0 +1,173 @@
+/*
+ * sldg.h -- C ABI of the B200-native mixed-precision semi-Lagrangian discontinuous Galerkin
+ * (SLDG) translate-and-project step of Einkemmer, "A mixed precision semi-Lagrangian
+ * algorithm and its performance on accelerators" (arXiv:1603.07008).
+ *
+ * Citation keys: P:NNN = /root/reference/PAPER.md line NNN (section in parentheses),
+ * S:NNN = SPEC.md line NNN (interface shapes only), SURVEY = /root/repo/SURVEY.md,
+ * R<n> = reading n in /root/repo/DESIGN.md.
+ *
+ * What the library computes (SS II-A):
+ *   Each cell of a periodic tensor-product grid (D = 1..6 dims, n_d cells along dim d,
+ *   width h_d = (hi_d - lo_d)/n_d) holds a modal Legendre expansion with k coefficients per
+ *   dim (k^D per cell, "u(x) ~ sum_j c_j P_j(2x/h)").  One advection sweep along
+ *   dim d translates the function exactly by nu*h_d (nu = CFL number in CELLS, per line)
+ *   and L2-projects it back:
+ *       c'_{i,j} = sum_l A_jl(alpha) c_{(i-i*-1) mod n, l} + sum_l B_jl(alpha) c_{(i-i*) mod n, l}
+ *   with i* = floor(nu), alpha = nu - i* (readings R1-R2), A and B the k x k
+ *   shift matrices, applied to the coefficient index along d while the
+ *   other indices are spectators (dimension splitting).  alpha = 0 is an exact
+ *   rotation (R4).
+ *
+ * Storage (R5): SLDG_MIXED keeps the all-zero multi-index coefficient (c_0, the
+ * cell mass) in fp64 and every other coefficient in fp32, rounded to nearest-even on every
+ * store; arithmetic is fp64 (R6).  SLDG_FP64 keeps all coefficients in fp64 (the baseline the
+ * paper compares against, Tables III-VI).
+ *
+ * Host coefficient layout used by set/get (fp64, all-or-nothing):
+ *   buf[c * K + q], K = k^D, c = local linear cell index = sum_d i_d * S_d with S_0 = 1,
+ *   S_d = prod_{e<d} n_e (dim 0 fastest; for a sharded grid i_{D-1} is the LOCAL layer index,
+ *   see sldg_shard_info), q = sum_d m_d k^d (m_0 fastest).
+ *
+ * Errors: every function returns sldg_status; no C++ exception crosses the ABI.
+ * sldg_last_error() returns a thread-local message for the last failure on this thread.
+ * EINVAL failures leave the grid unchanged.  Ownership: the handle owns all device memory
+ * it allocates (and the NCCL communicator if it created one); the caller owns all host
+ * buffers, which are never retained after a call returns.
+ * Threading: a handle is not thread-safe; distinct handles are independent.  When the grid
+ * is distributed (world > 1) every call except sldg_last_error / sldg_memory_bytes /
+ * sldg_shard_info is collective and must be made in the same order on all ranks.
+ * Streams: all device work is ordered on the handle's stream (its own non-blocking stream,
+ * or the one given to sldg_set_stream).  advect and fill_* are asynchronous; set_coeffs,
+ * get_coeffs, mass, sync and kernel_time block the host.
+ */
+#ifndef SLDG_H
+#define SLDG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLDG_MAX_DIM 6
+#define SLDG_MAX_K 8
+
+typedef struct sldg_grid_s* sldg_grid; /* opaque handle */
+
+typedef enum {
+    SLDG_OK = 0,
+    SLDG_EINVAL = 1,  /* invalid argument; no state changed                            */
+    SLDG_ENOMEM = 2,  /* device or pinned-host allocation failed               */
+    SLDG_ECUDA = 3,   /* CUDA runtime error; message in sldg_last_error()              */
+    SLDG_ENCCL = 4,   /* NCCL error; message in sldg_last_error()                      */
+    SLDG_ENOTSUP = 5  /* valid request this build does not support (e.g. halo > pad)   */
+} sldg_status;
+
+typedef enum {
+    SLDG_MIXED = 0, /* c_{0..0} fp64, all other coefficients fp32          */
+    SLDG_FP64 = 1   /* all coefficients fp64 (the paper's "double precision" baseline)  */
+} sldg_precision;
+
+typedef struct {
+    int ndim;                      /* D in 1..SLDG_MAX_DIM                                 */
+    int64_t cells[SLDG_MAX_DIM];   /* n_d >= 1 (GLOBAL extents); cells[0] is contiguous    */
+} sldg_grid_desc;
+
+typedef struct {
+    double lo[SLDG_MAX_DIM], hi[SLDG_MAX_DIM]; /* periodic box, h_d = (hi-lo)/n_d > 0      */
+} sldg_domain;
+
+/* Distribution over `world` GPUs (one process per GPU).  The outermost dim D-1 (D >= 2) is
+ * block-sharded: rank r owns global layers [r*n/world + min(r, n%world) ...) (balanced).
+ * Sweeps along dims < D-1 are communication-free; a sweep along D-1 exchanges halo layers
+ * with NCCL send/recv over NVLink.  Exactly one of nccl_unique_id / nccl_comm is non-NULL. */
+typedef struct {
+    int rank, world;
+    const void* nccl_unique_id; /* 128-byte ncclUniqueId, identical on all ranks, or NULL  */
+    void* nccl_comm;            /* caller-owned ncclComm_t (rank/world must match), or NULL */
+    int max_halo;               /* halo layers allocated per side; <= 0 selects 2          */
+} sldg_dist;
+
+/* Create a grid (zero-filled).  k in 1..SLDG_MAX_K coefficients per dim (the paper's order
+ * o = p+1).  dist may be NULL (single GPU).  The device is the caller's current
+ * CUDA device.  Errors: EINVAL (ndim, k, n_d < 1, lo >= hi, world/rank, sharded extent
+ * < world), ENOMEM, ECUDA, ENCCL. */
+sldg_status sldg_create(const sldg_grid_desc* grid, int k, const sldg_domain* dom,
+                        sldg_precision prec, const sldg_dist* dist, sldg_grid* out);
+sldg_status sldg_destroy(sldg_grid g);
+
+/* Copy n_cells cells starting at local cell first_cell from host fp64 (layout above) into
+ * the grid; fp32 slots are rounded to nearest-even.  Validation before any
+ * write (all-or-nothing): range inside the local shard; every value finite; every fp32
+ * slot |v| <= FLT_MAX.  Blocks until the copy is complete. */
+sldg_status sldg_set_coeffs(sldg_grid g, const double* src, int64_t first_cell, int64_t n_cells);
+/* Copy cells out to host fp64 (fp32 slots promoted exactly).  Blocks. */
+sldg_status sldg_get_coeffs(sldg_grid g, double* dst, int64_t first_cell, int64_t n_cells);
+
+/* One SLDG sweep along dim.  shift/field are CFL numbers in cells (R2).
+ * field == NULL: every line uses nu = shift.  Otherwise `field` (HOST memory) holds one nu
+ * per combination of the dims set in field_mask, indexed sum_{e in mask, ascending}
+ * i_e * prod_{e' in mask, e' < e} n_e' over GLOBAL indices; unmasked perpendicular dims
+ * broadcast (per-line variable CFL).  Errors (EINVAL, no state change): dim out
+ * of range, bit `dim` set in field_mask, mask bits >= D, non-finite or |nu| >= 2^62 entry
+ * (S:211).  ENOTSUP: sharded sweep whose halo exceeds max_halo.  Asynchronous. */
+sldg_status sldg_advect(sldg_grid g, int dim, double shift, const double* field, uint32_t field_mask);
+/* Same, with the field already resident in DEVICE memory (d_field, fp64, same indexing).
+ * Entries are validated on the device: a non-finite entry leaves its lines unchanged and
+ * makes the next blocking call return EINVAL (sticky device error). */
+sldg_status sldg_advect_device(sldg_grid g, int dim, double shift, const double* d_field,
+                               uint32_t field_mask);
+
+/* Total mass M = (prod_d h_d) * sum_cells c_{cell,0}, a deterministic
+ * fixed-order fp64 reduction; collective over ranks (rank-ordered sum).  Blocks. */
+sldg_status sldg_mass(sldg_grid g, double* mass_out);
+
+/* Local shard: first global layer along dim D-1 and number of local layers (1D: 0, 1). */
+sldg_status sldg_shard_info(sldg_grid g, int64_t* first_layer, int64_t* n_layers);
+sldg_status sldg_sync(sldg_grid g);
+/* Use an external CUDA stream (cudaStream_t) for all subsequent work (NULL = own stream). */
+sldg_status sldg_set_stream(sldg_grid g, void* cuda_stream);
+sldg_status sldg_get_stream(sldg_grid g, void** cuda_stream);
+/* Bytes of one coefficient array of the local shard: cells*(8+4(K-1)) mixed, cells*8K fp64
+ * (S:163-169); the library holds two (ping-pong) plus halo layers. */
+size_t sldg_memory_bytes(sldg_grid g);
+const char* sldg_last_error(void);
+
+/* ---- synthetic inputs; not part of the method ----------------------------- */
+/* Counter-based parity generator, bit-identical to sldg_inputs.random_coeffs:
+ * u = (splitmix64(seed*2^40 + g*K + q) >> 11) * 2^-53, r = 2u-1, c_0 = 1 + r/2,
+ * c_m = r / n_0^{|m|_1}; g = GLOBAL cell index.  Asynchronous. */
+sldg_status sldg_fill_random(sldg_grid g, uint64_t seed);
+/* c[cell,q] = sum_t prod_d T[t][d][i_d][m_d]; `tables` is HOST fp64, concatenated over
+ * t (n_terms) then d then [n_d global][k].  Used for Landau-type initial values. */
+sldg_status sldg_fill_separable(sldg_grid g, int n_terms, const double* tables);
+
+/* ---- instrumentation (for the bench harness) ------------------------------------------- */
+/* When enabled, CUDA events bracket every sweep kernel on the handle's stream. */
+sldg_status sldg_profile(sldg_grid g, int enable);
+/* Sum of sweep-kernel durations (ms) since the last reset for sweeps along `dim` (-1: all
+ * dims), their launch count, and the algorithmic bytes those launches moved (one load + one
+ * store per stored coefficient).  Blocks.  reset != 0 clears all accumulators. */
+sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches, double* bytes, int reset);
+/* Number of kernels this handle has launched (all kinds). */
+int64_t sldg_launch_count(sldg_grid g);
+
+/* ---- distributed helpers ---------------------------------------------------------------- */
+/* Write a fresh 128-byte ncclUniqueId into out128 (call on rank 0, broadcast it). */
+sldg_status sldg_nccl_unique_id(void* out128);
+/* Host-only halo planner for a sweep along the sharded dim (no device, no NCCL):
+ * given global extent n, world, rank and the integer-shift range [imin, imax] of the
+ * sweep's lines (i* = floor(nu)), returns the halo widths this rank needs on the left
+ * (layers below its first layer) and right.  Lines with integer part i* read layers
+ * i - i* - 1 and i - i*, so left = max(0, imax + 1), right = max(0, -imin). */
+sldg_status sldg_halo_widths(int64_t imin, int64_t imax, int64_t* left, int64_t* right);
+/* Owner rank and local index of global layer `layer` in a balanced block split of n over
+ * world ranks. */
+sldg_status sldg_layer_owner(int64_t n, int world, int64_t layer, int* owner, int64_t* local);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLDG_H */

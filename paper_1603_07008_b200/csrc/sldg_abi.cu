@@ -1,0 +1,750 @@
+// sldg_abi.cu -- host side of the C ABI declared in include/sldg.h.
+//
+// Owns device memory (two coefficient arrays for ping-pong, weight tables, staging), the
+// CUDA stream, the optional NCCL communicator, and the sweep sequencing:
+//   validate -> upload field -> build weights (a1, a2) -> [halo exchange] -> sweep (a3-a7)
+//   -> swap buffers.
+#include <cuda_runtime.h>
+#include <float.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <algorithm>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "sldg_internal.h"
+
+using namespace sldg;
+
+struct sldg_grid_s : public Grid {
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+    int64_t* d_range = nullptr;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+sldg_status fail(sldg_status st, const std::string& msg)
+{
+    g_last_error = msg;
+    return st;
+}
+
+#define CU(call)                                                                                   \
+    do {                                                                                           \
+        cudaError_t e_ = (call);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(e_ == cudaErrorMemoryAllocation ? SLDG_ENOMEM : SLDG_ECUDA,                \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                       \
+    } while (0)
+
+#define NC(call)                                                                                   \
+    do {                                                                                           \
+        ncclResult_t r_ = (call);                                                                  \
+        if (r_ != ncclSuccess) return fail(SLDG_ENCCL, std::string(#call) + ": " + ncclGetErrorString(r_)); \
+    } while (0)
+
+// Balanced block split of n layers over world ranks.
+void split(int64_t n, int world, int rank, int64_t* first, int64_t* count)
+{
+    int64_t base = n / world, extra = n % world;
+    *count = base + (rank < extra ? 1 : 0);
+    *first = rank * base + std::min<int64_t>(rank, extra);
+}
+
+int owner_of(int64_t n, int world, int64_t layer, int64_t* local)
+{
+    for (int r = 0; r < world; ++r) {
+        int64_t f, c;
+        split(n, world, r, &f, &c);
+        if (layer >= f && layer < f + c) {
+            if (local) *local = layer - f;
+            return r;
+        }
+    }
+    return -1;
+}
+
+size_t bytes_per_cell(const Layout& L)
+{
+    return L.prec == SLDG_FP64 ? (size_t)8 * L.K : (size_t)8 + (size_t)4 * (L.K - 1);
+}
+
+Arrays arrays_of(const Layout& L, void* base)
+{
+    Arrays a;
+    const size_t rows = (size_t)(L.layers + 2 * L.pad) * (size_t)L.L;
+    if (L.prec == SLDG_FP64) {
+        a.s64 = (double*)base;
+    } else {
+        a.mass = (double*)base;
+        size_t off = ((rows * 8 + 255) / 256) * 256;
+        a.pl = (float*)((char*)base + off);
+    }
+    return a;
+}
+
+size_t array_alloc_bytes(const Layout& L)
+{
+    const size_t rows = (size_t)(L.layers + 2 * L.pad) * (size_t)L.L;
+    if (L.prec == SLDG_FP64) return rows * 8 * (size_t)L.K;
+    return ((rows * 8 + 255) / 256) * 256 + rows * 4 * (size_t)(L.K - 1);
+}
+
+sldg_status ensure_weights(sldg_grid g, int64_t n_entries)
+{
+    if (g->w.cap >= n_entries) return SLDG_OK;
+    cudaFree(g->w.shift);
+    cudaFree(g->w.smod);
+    cudaFree(g->w.copy);
+    cudaFree(g->w.ab);
+    g->w = Weights{};
+    int64_t cap = std::max<int64_t>(n_entries, 64);
+    const int k = g->lay.k;
+    CU(cudaMalloc(&g->w.shift, cap * sizeof(int64_t)));
+    CU(cudaMalloc(&g->w.smod, cap * sizeof(int64_t)));
+    CU(cudaMalloc(&g->w.copy, cap * sizeof(int)));
+    CU(cudaMalloc(&g->w.ab, cap * 2 * k * k * sizeof(double)));
+    g->w.cap = cap;
+    return SLDG_OK;
+}
+
+sldg_status ensure_field(sldg_grid g, int64_t n)
+{
+    if (g->field_cap >= n) return SLDG_OK;
+    cudaFree(g->d_field);
+    g->d_field = nullptr;
+    g->field_cap = 0;
+    int64_t cap = std::max<int64_t>(n, 64);
+    CU(cudaMalloc(&g->d_field, cap * sizeof(double)));
+    g->field_cap = cap;
+    return SLDG_OK;
+}
+
+sldg_status ensure_stage(sldg_grid g)
+{
+    if (g->d_stage) return SLDG_OK;
+    const size_t elems = (size_t)1 << 23;  // 64 MiB of fp64 per chunk
+    CU(cudaMalloc(&g->d_stage, elems * sizeof(double)));
+    CU(cudaMallocHost(&g->h_stage, elems * sizeof(double)));
+    g->stage_elems = elems;
+    return SLDG_OK;
+}
+
+sldg_status check_device_error(sldg_grid g)
+{
+    int err = 0;
+    CU(cudaMemcpyAsync(&err, g->d_err, sizeof(int), cudaMemcpyDeviceToHost, g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    if (err) {
+        CU(cudaMemsetAsync(g->d_err, 0, sizeof(int), g->stream));
+        return fail(SLDG_EINVAL, "a device-resident shift field held a non-finite or |nu| >= 2^62 entry; "
+                                 "its lines were left unchanged");
+    }
+    return SLDG_OK;
+}
+
+cudaEvent_t pool_event(sldg_grid g)
+{
+    if (!g->ev_pool.empty()) {
+        cudaEvent_t e = g->ev_pool.back();
+        g->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Launch one sweep kernel over local layers [lb, le) with optional profiling events.
+sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arrays& dst, int64_t lb, int64_t le)
+{
+    if (le <= lb) return SLDG_OK;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g->profile) {
+        e0 = pool_event(g);
+        e1 = pool_event(g);
+        CU(cudaEventRecord(e0, g->stream));
+    }
+    int nl = 0;
+    CU(launch_sweep(g->lay, sw, src, dst, lb, le, g->stream, &nl));
+    g->launches += nl;
+    if (g->profile) {
+        CU(cudaEventRecord(e1, g->stream));
+        g->ev_pairs.push_back({e0, e1});
+        g->ev_bytes.push_back(2.0 * (double)bytes_per_cell(g->lay) * (double)((le - lb) * g->lay.L));
+        g->ev_dim.push_back(sw.dim);
+    }
+    return SLDG_OK;
+}
+
+// Halo exchange along the sharded layer dim: this rank receives global layers
+// [first-left, first) and [first+layers, first+layers+right) (mod n) into its pad region of
+// `a`, and sends whatever other ranks need from its own layers.  Grouped NCCL send/recv on
+// the comm stream (two adjacent source cells => halo of ceil|nu| layers).
+sldg_status halo_exchange(sldg_grid g, const Arrays& a, int64_t left, int64_t right)
+{
+    const Layout& L = g->lay;
+    const int64_t n = L.n[L.D - 1];
+    ncclComm_t comm = (ncclComm_t)g->comm;
+    const size_t mass_elems = (size_t)L.L;
+    const size_t pl_elems = (size_t)L.L * (size_t)(L.K - 1);
+    const size_t s64_elems = (size_t)L.L * (size_t)L.K;
+    auto layer_ptrs = [&](int64_t lp, void** p0, size_t* c0, void** p1, size_t* c1) {
+        if (L.prec == SLDG_FP64) {
+            *p0 = a.s64 + (size_t)lp * s64_elems;
+            *c0 = s64_elems;
+            *p1 = nullptr;
+            *c1 = 0;
+        } else {
+            *p0 = a.mass + (size_t)lp * mass_elems;
+            *c0 = mass_elems;
+            *p1 = a.pl + (size_t)lp * pl_elems;
+            *c1 = pl_elems;
+        }
+    };
+    struct Xfer {
+        int peer;
+        int64_t lp;  // padded local layer index
+        bool send;
+    };
+    std::vector<Xfer> xs;
+    // receives: my halo slots
+    for (int64_t j = 0; j < left + right; ++j) {
+        int64_t gl, slot;
+        if (j < left) {
+            gl = L.first_layer - left + j;
+            slot = L.pad - left + j;
+        } else {
+            gl = L.first_layer + L.layers + (j - left);
+            slot = L.pad + L.layers + (j - left);
+        }
+        gl = ((gl % n) + n) % n;
+        int64_t loc = 0;
+        int own = owner_of(n, g->world, gl, &loc);
+        if (own == g->rank) {
+            void *d0, *d1, *s0, *s1;
+            size_t c0, c1;
+            layer_ptrs(slot, &d0, &c0, &d1, &c1);
+            layer_ptrs(L.pad + loc, &s0, &c0, &s1, &c1);
+            CU(cudaMemcpyAsync(d0, s0, c0 * (L.prec == SLDG_FP64 ? 8 : 8), cudaMemcpyDeviceToDevice, g->comm_stream));
+            if (d1) CU(cudaMemcpyAsync(d1, s1, c1 * 4, cudaMemcpyDeviceToDevice, g->comm_stream));
+        } else {
+            xs.push_back({own, slot, false});
+        }
+    }
+    // sends: for every other rank, the layers of mine it needs (same formula, their view)
+    for (int p = 0; p < g->world; ++p) {
+        if (p == g->rank) continue;
+        int64_t pf, pc;
+        split(n, g->world, p, &pf, &pc);
+        for (int64_t j = 0; j < left + right; ++j) {
+            int64_t gl = (j < left) ? pf - left + j : pf + pc + (j - left);
+            gl = ((gl % n) + n) % n;
+            int64_t loc = 0;
+            if (owner_of(n, g->world, gl, &loc) == g->rank) xs.push_back({p, L.pad + loc, true});
+        }
+    }
+    if (xs.empty()) return SLDG_OK;
+    NC(ncclGroupStart());
+    for (const Xfer& x : xs) {
+        void *p0, *p1;
+        size_t c0, c1;
+        layer_ptrs(x.lp, &p0, &c0, &p1, &c1);
+        if (x.send) {
+            NC(ncclSend(p0, c0, ncclFloat64, x.peer, comm, g->comm_stream));
+            if (p1) NC(ncclSend(p1, c1, ncclFloat32, x.peer, comm, g->comm_stream));
+        } else {
+            NC(ncclRecv(p0, c0, ncclFloat64, x.peer, comm, g->comm_stream));
+            if (p1) NC(ncclRecv(p1, c1, ncclFloat32, x.peer, comm, g->comm_stream));
+        }
+    }
+    NC(ncclGroupEnd());
+    return SLDG_OK;
+}
+
+sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field, bool field_on_device,
+                        uint32_t mask)
+{
+    const Layout& L = g->lay;
+    if (dim < 0 || dim >= L.D) return fail(SLDG_EINVAL, "dim out of range");
+    if (mask >> L.D) return fail(SLDG_EINVAL, "field_mask has bits >= ndim");
+    if (field && (mask & (1u << dim))) return fail(SLDG_EINVAL, "field_mask contains the advected dim");
+    if (!field && mask) return fail(SLDG_EINVAL, "field_mask given without a field");
+    int64_t n_entries = 1;
+    Sweep sw{};
+    sw.dim = dim;
+    sw.nd = L.n[dim];
+    sw.fmask = field ? mask : 0;
+    {
+        int64_t st = 1;
+        for (int e = 0; e < kMaxDim; ++e) {
+            sw.fstride[e] = 0;
+            if (e < L.D && (sw.fmask >> e & 1u)) {
+                sw.fstride[e] = st;
+                st *= L.n[e];
+            }
+        }
+        n_entries = st;
+    }
+    const bool sharded_sweep = (g->world > 1 && dim == L.D - 1);
+    int64_t imin = 0, imax = 0;
+    if (!field) {
+        if (!(fabs(shift) < 4.611686018427387904e18)) return fail(SLDG_EINVAL, "non-finite or huge shift");
+        double fl = floor(shift);
+        imin = imax = (int64_t)fl + ((shift - fl >= 1.0) ? 1 : 0);
+    } else if (!field_on_device) {
+        imin = INT64_MAX;
+        imax = INT64_MIN;
+        for (int64_t e = 0; e < n_entries; ++e) {
+            double nu = field[e];
+            if (!(fabs(nu) < 4.611686018427387904e18))
+                return fail(SLDG_EINVAL, "non-finite or |nu| >= 2^62 entry in shift field");
+            double fl = floor(nu);
+            int64_t is = (int64_t)fl + ((nu - fl >= 1.0) ? 1 : 0);
+            imin = std::min(imin, is);
+            imax = std::max(imax, is);
+        }
+    }
+    sldg_status st = ensure_weights(g, n_entries);
+    if (st != SLDG_OK) return st;
+    const double* dfield = nullptr;
+    if (field) {
+        if (field_on_device) {
+            dfield = field;
+        } else {
+            st = ensure_field(g, n_entries);
+            if (st != SLDG_OK) return st;
+            CU(cudaMemcpyAsync(g->d_field, field, n_entries * sizeof(double), cudaMemcpyHostToDevice, g->stream));
+            dfield = g->d_field;
+        }
+    }
+    if (sharded_sweep && field && field_on_device) {
+        CU(launch_field_range(dfield, n_entries, shift, g->d_range, g->stream));
+        int64_t r[2];
+        CU(cudaMemcpyAsync(r, g->d_range, sizeof(r), cudaMemcpyDeviceToHost, g->stream));
+        CU(cudaStreamSynchronize(g->stream));
+        imin = r[0];
+        imax = r[1];
+        if (imin > imax) imin = imax = 0;  // all entries invalid: lines are copied (error sticky)
+    }
+    CU(launch_weights(L, sw.nd, dfield, shift, n_entries, g->w, g->d_err, g->stream));
+    g->launches += 1;
+    sw.shift = g->w.shift;
+    sw.smod = g->w.smod;
+    sw.copy = g->w.copy;
+    sw.ab = g->w.ab;
+
+    const Arrays& src = g->buf[g->cur];
+    const Arrays& dst = g->buf[1 - g->cur];
+    if (!sharded_sweep) {
+        sw.wrap = 1;
+        st = run_sweep(g, sw, src, dst, 0, L.layers);
+        if (st != SLDG_OK) return st;
+    } else {
+        int64_t left = std::max<int64_t>(0, imax + 1), right = std::max<int64_t>(0, -imin);
+        if (left > L.pad || right > L.pad)
+            return fail(SLDG_ENOTSUP, "halo of " + std::to_string(std::max(left, right)) +
+                                          " layers exceeds max_halo=" + std::to_string(L.pad));
+        sw.wrap = 0;
+        CU(cudaEventRecord(g->ev_ready, g->stream));
+        CU(cudaStreamWaitEvent(g->comm_stream, g->ev_ready, 0));
+        st = halo_exchange(g, src, left, right);
+        if (st != SLDG_OK) return st;
+        CU(cudaEventRecord(g->ev_halo, g->comm_stream));
+        // interior layers need no halo: overlap them with the exchange
+        int64_t ib = std::min(left, L.layers), ie = std::max(ib, L.layers - right);
+        st = run_sweep(g, sw, src, dst, ib, ie);
+        if (st != SLDG_OK) return st;
+        CU(cudaStreamWaitEvent(g->stream, g->ev_halo, 0));
+        st = run_sweep(g, sw, src, dst, 0, ib);
+        if (st != SLDG_OK) return st;
+        st = run_sweep(g, sw, src, dst, ie, L.layers);
+        if (st != SLDG_OK) return st;
+    }
+    g->cur = 1 - g->cur;
+    return SLDG_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sldg_last_error(void) { return g_last_error.c_str(); }
+
+sldg_status sldg_nccl_unique_id(void* out128)
+{
+    if (!out128) return fail(SLDG_EINVAL, "null output");
+    ncclUniqueId id;
+    NC(ncclGetUniqueId(&id));
+    static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+    memcpy(out128, &id, 128);
+    return SLDG_OK;
+}
+
+sldg_status sldg_halo_widths(int64_t imin, int64_t imax, int64_t* left, int64_t* right)
+{
+    if (!left || !right || imin > imax) return fail(SLDG_EINVAL, "bad arguments");
+    *left = std::max<int64_t>(0, imax + 1);
+    *right = std::max<int64_t>(0, -imin);
+    return SLDG_OK;
+}
+
+sldg_status sldg_layer_owner(int64_t n, int world, int64_t layer, int* owner, int64_t* local)
+{
+    if (n < 1 || world < 1 || world > n || layer < 0 || layer >= n || !owner)
+        return fail(SLDG_EINVAL, "bad arguments");
+    *owner = owner_of(n, world, layer, local);
+    return SLDG_OK;
+}
+
+sldg_status sldg_create(const sldg_grid_desc* grid, int k, const sldg_domain* dom, sldg_precision prec,
+                        const sldg_dist* dist, sldg_grid* out)
+{
+    if (!grid || !dom || !out) return fail(SLDG_EINVAL, "null argument");
+    *out = nullptr;
+    if (grid->ndim < 1 || grid->ndim > SLDG_MAX_DIM) return fail(SLDG_EINVAL, "ndim must be in 1..6");
+    if (k < 1 || k > SLDG_MAX_K) return fail(SLDG_EINVAL, "k must be in 1..8");
+    if (prec != SLDG_MIXED && prec != SLDG_FP64) return fail(SLDG_EINVAL, "bad precision");
+    const int D = grid->ndim;
+    int64_t K = 1;
+    for (int d = 0; d < D; ++d) {
+        if (grid->cells[d] < 1) return fail(SLDG_EINVAL, "cells must be >= 1");
+        if (!(dom->hi[d] > dom->lo[d]) || !isfinite(dom->lo[d]) || !isfinite(dom->hi[d]))
+            return fail(SLDG_EINVAL, "domain must have lo < hi (finite)");
+        K *= k;
+    }
+    if (K > (1 << 20)) return fail(SLDG_EINVAL, "k^D too large");
+    int rank = 0, world = 1;
+    if (dist) {
+        rank = dist->rank;
+        world = dist->world;
+        if (world < 1 || rank < 0 || rank >= world) return fail(SLDG_EINVAL, "bad rank/world");
+        if (world > 1 && D < 2) return fail(SLDG_EINVAL, "a 1D grid cannot be sharded");
+        if (world > 1 && grid->cells[D - 1] < world)
+            return fail(SLDG_EINVAL, "sharded extent smaller than world");
+        if (world > 1 && !dist->nccl_unique_id && !dist->nccl_comm)
+            return fail(SLDG_EINVAL, "distributed grid needs an ncclUniqueId or ncclComm");
+    }
+    sldg_grid g = new (std::nothrow) sldg_grid_s();
+    if (!g) return fail(SLDG_ENOMEM, "host allocation failed");
+    Layout& L = g->lay;
+    L.D = D;
+    L.k = k;
+    L.K = (int)K;
+    L.prec = prec;
+    int64_t S = 1;
+    for (int d = 0; d < kMaxDim; ++d) {
+        L.n[d] = d < D ? grid->cells[d] : 1;
+        L.S[d] = S;
+        if (d < D) {
+            g->lo[d] = dom->lo[d];
+            g->hi[d] = dom->hi[d];
+            g->h[d] = (dom->hi[d] - dom->lo[d]) / (double)grid->cells[d];
+            S *= grid->cells[d];
+        } else {
+            g->lo[d] = 0.0;
+            g->hi[d] = 1.0;
+            g->h[d] = 1.0;
+        }
+    }
+    if (D == 1) {
+        L.L = L.n[0];
+        L.layers = 1;
+        L.first_layer = 0;
+    } else {
+        L.L = 1;
+        for (int d = 0; d < D - 1; ++d) L.L *= L.n[d];
+        split(L.n[D - 1], world, rank, &L.first_layer, &L.layers);
+    }
+    L.pad = (world > 1) ? ((dist->max_halo > 0) ? dist->max_halo : 2) : 0;
+    L.cells = L.layers * L.L;
+    g->rank = rank;
+    g->world = world;
+
+    auto bail = [&](sldg_status st) {
+        sldg_destroy(g);
+        return st;
+    };
+    if (cudaGetDevice(&g->device) != cudaSuccess) return bail(fail(SLDG_ECUDA, "no CUDA device"));
+    if (cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking) != cudaSuccess)
+        return bail(fail(SLDG_ECUDA, "stream create failed"));
+    g->own_stream = true;
+    if (cudaStreamCreateWithFlags(&g->comm_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g->ev_halo, cudaEventDisableTiming) != cudaSuccess)
+        return bail(fail(SLDG_ECUDA, "stream/event create failed"));
+    g->alloc_bytes = array_alloc_bytes(L);
+    for (int b = 0; b < 2; ++b) {
+        cudaError_t e = cudaMalloc(&g->alloc[b], g->alloc_bytes);
+        if (e != cudaSuccess)
+            return bail(fail(SLDG_ENOMEM, "device allocation of " + std::to_string(g->alloc_bytes) +
+                                              " bytes failed: " + cudaGetErrorString(e)));
+        if (cudaMemsetAsync(g->alloc[b], 0, g->alloc_bytes, g->stream) != cudaSuccess)
+            return bail(fail(SLDG_ECUDA, "memset failed"));
+        g->buf[b] = arrays_of(L, g->alloc[b]);
+    }
+    if (cudaMalloc(&g->d_partials, kMassBlocks * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&g->d_scalar, 64 * sizeof(double)) != cudaSuccess ||
+        cudaMalloc(&g->d_err, sizeof(int)) != cudaSuccess ||
+        cudaMalloc(&g->d_range, 2 * sizeof(int64_t)) != cudaSuccess)
+        return bail(fail(SLDG_ENOMEM, "device allocation failed"));
+    if (cudaMemsetAsync(g->d_err, 0, sizeof(int), g->stream) != cudaSuccess)
+        return bail(fail(SLDG_ECUDA, "memset failed"));
+    if (world > 1) {
+        if (dist->nccl_comm) {
+            g->comm = dist->nccl_comm;
+            g->own_comm = false;
+        } else {
+            ncclUniqueId id;
+            memcpy(&id, dist->nccl_unique_id, sizeof(id));
+            ncclComm_t c;
+            ncclResult_t r = ncclCommInitRank(&c, world, id, rank);
+            if (r != ncclSuccess) return bail(fail(SLDG_ENCCL, std::string("ncclCommInitRank: ") + ncclGetErrorString(r)));
+            g->comm = c;
+            g->own_comm = true;
+        }
+    }
+    if (cudaStreamSynchronize(g->stream) != cudaSuccess) return bail(fail(SLDG_ECUDA, "sync failed"));
+    *out = g;
+    return SLDG_OK;
+}
+
+sldg_status sldg_destroy(sldg_grid g)
+{
+    if (!g) return SLDG_OK;
+    if (g->stream) cudaStreamSynchronize(g->stream);
+    if (g->comm_stream) cudaStreamSynchronize(g->comm_stream);
+    if (g->own_comm && g->comm) ncclCommDestroy((ncclComm_t)g->comm);
+    for (int b = 0; b < 2; ++b) cudaFree(g->alloc[b]);
+    cudaFree(g->w.shift);
+    cudaFree(g->w.smod);
+    cudaFree(g->w.copy);
+    cudaFree(g->w.ab);
+    cudaFree(g->d_field);
+    cudaFree(g->d_partials);
+    cudaFree(g->d_scalar);
+    cudaFree(g->d_err);
+    cudaFree(g->d_range);
+    cudaFree(g->d_stage);
+    if (g->h_stage) cudaFreeHost(g->h_stage);
+    for (auto& p : g->ev_pairs) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
+    for (auto e : g->ev_pool) cudaEventDestroy(e);
+    if (g->ev_ready) cudaEventDestroy(g->ev_ready);
+    if (g->ev_halo) cudaEventDestroy(g->ev_halo);
+    if (g->comm_stream) cudaStreamDestroy(g->comm_stream);
+    if (g->own_stream && g->stream) cudaStreamDestroy(g->stream);
+    delete g;
+    return SLDG_OK;
+}
+
+sldg_status sldg_set_coeffs(sldg_grid g, const double* src, int64_t first_cell, int64_t n_cells)
+{
+    if (!g || (!src && n_cells > 0)) return fail(SLDG_EINVAL, "null argument");
+    const Layout& L = g->lay;
+    if (first_cell < 0 || n_cells < 0 || first_cell + n_cells > L.cells)
+        return fail(SLDG_EINVAL, "cell range outside the local shard");
+    const int64_t n = n_cells * L.K;
+    for (int64_t e = 0; e < n; ++e) {  // all-or-nothing validation
+        double v = src[e];
+        if (!isfinite(v)) return fail(SLDG_EINVAL, "non-finite coefficient at element " + std::to_string(e));
+        if (L.prec == SLDG_MIXED && (e % L.K) != 0 && fabs(v) > (double)FLT_MAX)
+            return fail(SLDG_EINVAL, "value beyond FLT_MAX in an fp32 slot at element " + std::to_string(e));
+    }
+    sldg_status st = ensure_stage(g);
+    if (st != SLDG_OK) return st;
+    const int64_t chunk_cells = (int64_t)g->stage_elems / L.K;
+    for (int64_t c0 = 0; c0 < n_cells; c0 += chunk_cells) {
+        int64_t nc = std::min(chunk_cells, n_cells - c0);
+        memcpy(g->h_stage, src + c0 * L.K, (size_t)nc * L.K * sizeof(double));
+        CU(cudaMemcpyAsync(g->d_stage, g->h_stage, (size_t)nc * L.K * sizeof(double), cudaMemcpyHostToDevice, g->stream));
+        CU(launch_set(L, g->buf[g->cur], g->d_stage, first_cell + c0, nc, g->stream));
+        g->launches += 1;
+        CU(cudaStreamSynchronize(g->stream));
+    }
+    return SLDG_OK;
+}
+
+sldg_status sldg_get_coeffs(sldg_grid g, double* dst, int64_t first_cell, int64_t n_cells)
+{
+    if (!g || (!dst && n_cells > 0)) return fail(SLDG_EINVAL, "null argument");
+    const Layout& L = g->lay;
+    if (first_cell < 0 || n_cells < 0 || first_cell + n_cells > L.cells)
+        return fail(SLDG_EINVAL, "cell range outside the local shard");
+    sldg_status st = ensure_stage(g);
+    if (st != SLDG_OK) return st;
+    const int64_t chunk_cells = (int64_t)g->stage_elems / L.K;
+    for (int64_t c0 = 0; c0 < n_cells; c0 += chunk_cells) {
+        int64_t nc = std::min(chunk_cells, n_cells - c0);
+        CU(launch_get(L, g->buf[g->cur], g->d_stage, first_cell + c0, nc, g->stream));
+        g->launches += 1;
+        CU(cudaMemcpyAsync(g->h_stage, g->d_stage, (size_t)nc * L.K * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+        CU(cudaStreamSynchronize(g->stream));
+        memcpy(dst + c0 * L.K, g->h_stage, (size_t)nc * L.K * sizeof(double));
+    }
+    return check_device_error(g);
+}
+
+sldg_status sldg_advect(sldg_grid g, int dim, double shift, const double* field, uint32_t field_mask)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    return advect_impl(g, dim, shift, field, false, field_mask);
+}
+
+sldg_status sldg_advect_device(sldg_grid g, int dim, double shift, const double* d_field, uint32_t field_mask)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    return advect_impl(g, dim, shift, d_field, true, field_mask);
+}
+
+sldg_status sldg_mass(sldg_grid g, double* mass_out)
+{
+    if (!g || !mass_out) return fail(SLDG_EINVAL, "null argument");
+    const Layout& L = g->lay;
+    CU(launch_mass_partials(L, g->buf[g->cur], g->d_partials, g->d_scalar, g->stream));
+    g->launches += 2;
+    double vol = 1.0;
+    for (int d = 0; d < L.D; ++d) vol *= g->h[d];
+    std::vector<double> parts((size_t)g->world, 0.0);
+    if (g->world > 1) {
+        NC(ncclAllGather(g->d_scalar, g->d_scalar + 1, 1, ncclFloat64, (ncclComm_t)g->comm, g->stream));
+        CU(cudaMemcpyAsync(parts.data(), g->d_scalar + 1, g->world * sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+    } else {
+        CU(cudaMemcpyAsync(parts.data(), g->d_scalar, sizeof(double), cudaMemcpyDeviceToHost, g->stream));
+    }
+    CU(cudaStreamSynchronize(g->stream));
+    double s = 0.0;
+    for (int r = 0; r < g->world; ++r) s += parts[r];  // rank-ordered
+    *mass_out = vol * s;
+    return check_device_error(g);
+}
+
+sldg_status sldg_shard_info(sldg_grid g, int64_t* first_layer, int64_t* n_layers)
+{
+    if (!g || !first_layer || !n_layers) return fail(SLDG_EINVAL, "null argument");
+    *first_layer = g->lay.first_layer;
+    *n_layers = g->lay.layers;
+    return SLDG_OK;
+}
+
+sldg_status sldg_sync(sldg_grid g)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    CU(cudaStreamSynchronize(g->stream));
+    CU(cudaStreamSynchronize(g->comm_stream));
+    return check_device_error(g);
+}
+
+sldg_status sldg_set_stream(sldg_grid g, void* cuda_stream)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    CU(cudaStreamSynchronize(g->stream));
+    if (g->own_stream) cudaStreamDestroy(g->stream);
+    if (cuda_stream) {
+        g->stream = (cudaStream_t)cuda_stream;
+        g->own_stream = false;
+    } else {
+        CU(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        g->own_stream = true;
+    }
+    return SLDG_OK;
+}
+
+sldg_status sldg_get_stream(sldg_grid g, void** cuda_stream)
+{
+    if (!g || !cuda_stream) return fail(SLDG_EINVAL, "null argument");
+    *cuda_stream = (void*)g->stream;
+    return SLDG_OK;
+}
+
+size_t sldg_memory_bytes(sldg_grid g)
+{
+    if (!g) return 0;
+    return (size_t)g->lay.cells * bytes_per_cell(g->lay);
+}
+
+sldg_status sldg_fill_random(sldg_grid g, uint64_t seed)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    CU(launch_fill_random(g->lay, g->buf[g->cur], seed, g->stream));
+    g->launches += 1;
+    return SLDG_OK;
+}
+
+sldg_status sldg_fill_separable(sldg_grid g, int n_terms, const double* tables)
+{
+    if (!g || !tables || n_terms < 1) return fail(SLDG_EINVAL, "bad arguments");
+    const Layout& L = g->lay;
+    int64_t per_term = 0;
+    for (int d = 0; d < L.D; ++d) per_term += L.n[d] * L.k;
+    const size_t bytes = (size_t)per_term * n_terms * sizeof(double);
+    for (size_t e = 0; e < (size_t)per_term * n_terms; ++e)
+        if (!isfinite(tables[e])) return fail(SLDG_EINVAL, "non-finite table entry");
+    double* d_tab = nullptr;
+    CU(cudaMallocAsync((void**)&d_tab, bytes, g->stream));
+    CU(cudaMemcpyAsync(d_tab, tables, bytes, cudaMemcpyHostToDevice, g->stream));
+    CU(launch_fill_separable(L, g->buf[g->cur], n_terms, d_tab, g->stream));
+    g->launches += 1;
+    CU(cudaFreeAsync(d_tab, g->stream));
+    CU(cudaStreamSynchronize(g->stream));
+    return SLDG_OK;
+}
+
+sldg_status sldg_profile(sldg_grid g, int enable)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    g->profile = enable != 0;
+    return SLDG_OK;
+}
+
+sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches, double* bytes, int reset)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    if (dim < -1 || dim >= g->lay.D) return fail(SLDG_EINVAL, "dim out of range");
+    CU(cudaStreamSynchronize(g->stream));
+    for (size_t i = 0; i < g->ev_pairs.size(); ++i) {
+        float t = 0.f;
+        CU(cudaEventElapsedTime(&t, g->ev_pairs[i].first, g->ev_pairs[i].second));
+        const int d = g->ev_dim[i];
+        g->prof_ms[d] += t;
+        g->prof_bytes[d] += g->ev_bytes[i];
+        g->prof_launches[d] += 1;
+        g->ev_pool.push_back(g->ev_pairs[i].first);
+        g->ev_pool.push_back(g->ev_pairs[i].second);
+    }
+    g->ev_pairs.clear();
+    g->ev_bytes.clear();
+    g->ev_dim.clear();
+    double m = 0.0, b = 0.0;
+    int64_t n = 0;
+    for (int d = 0; d < g->lay.D; ++d) {
+        if (dim >= 0 && d != dim) continue;
+        m += g->prof_ms[d];
+        b += g->prof_bytes[d];
+        n += g->prof_launches[d];
+    }
+    if (ms) *ms = m;
+    if (launches) *launches = n;
+    if (bytes) *bytes = b;
+    if (reset) {
+        for (int d = 0; d < kMaxDim; ++d) {
+            g->prof_ms[d] = 0.0;
+            g->prof_bytes[d] = 0.0;
+            g->prof_launches[d] = 0;
+        }
+    }
+    return SLDG_OK;
+}
+
+int64_t sldg_launch_count(sldg_grid g) { return g ? g->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+// sldg_internal.h -- internal types of the B200 SLDG library (not part of the ABI).
+//
+// Device layout of one coefficient array:
+//   The outermost dim D-1 (D >= 2) is the LAYER dim (sharded across ranks); a layer holds
+//   L = prod_{d<D-1} n_d cells.  For D == 1 there is one virtual layer with L = n_0.
+//   mixed : mass[(pad + layer) * L + inner]                        (fp64, slot q = 0)
+//           pl  [((pad + layer) * (K-1) + (q-1)) * L + inner]       (fp32, slots q >= 1)
+//   fp64  : s64 [((pad + layer) * K + q) * L + inner]                (fp64, all slots)
+//   inner = sum_{d<D-1} i_d S_d.  One layer of all slots is contiguous per array, so a halo
+//   layer is two contiguous chunks (mixed) or one (fp64).  `pad` layers on each side hold
+//   halos when the layer dim is sharded.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/sldg.h"
+
+namespace sldg {
+
+constexpr int kMaxDim = SLDG_MAX_DIM;
+constexpr int kMaxK = SLDG_MAX_K;
+
+// One coefficient array (a ping-pong buffer).
+struct Arrays {
+    double* mass = nullptr;  // mixed: fp64 slot 0
+    float* pl = nullptr;     // mixed: fp32 slots 1..K-1
+    double* s64 = nullptr;   // fp64 variant: all slots
+};
+
+// Per-sweep weight table: one entry per field entry (or a single one for a constant shift).
+struct Weights {
+    int64_t* shift = nullptr;  // i* (raw) per entry
+    int64_t* smod = nullptr;   // i* mod n_d in [0, n_d) per entry
+    int* copy = nullptr;       // 1 if alpha == 0 (exact rotation)
+    double* ab = nullptr;      // [entry][2][k][k]: A then B, row-major
+    int64_t cap = 0;
+};
+
+// Layout + sweep description passed by value to the kernels.
+struct Layout {
+    int D;
+    int k;
+    int K;            // k^D
+    int prec;         // SLDG_MIXED / SLDG_FP64
+    int64_t n[kMaxDim];   // GLOBAL extents
+    int64_t S[kMaxDim];   // inner strides S_d (d < D-1); S_{D-1} unused
+    int64_t L;            // cells per layer
+    int64_t layers;       // local layers
+    int64_t first_layer;  // global index of local layer 0
+    int64_t pad;          // halo layers per side
+    int64_t cells;        // local cells = layers * L
+};
+
+struct Sweep {
+    int dim;
+    int64_t nd;                // extent along dim (global)
+    uint32_t fmask;
+    int64_t fstride[kMaxDim];  // field index stride per dim (0 if not masked)
+    int wrap;                  // 1: periodic modulo indexing; 0: read halos (layer dim sharded)
+    const int64_t* shift;  // raw i*
+    const int64_t* smod;   // i* mod nd
+    const int* copy;
+    const double* ab;
+};
+
+struct Grid {
+    Layout lay;
+    double h[kMaxDim];
+    double lo[kMaxDim], hi[kMaxDim];
+    Arrays buf[2];
+    int cur = 0;
+    void* alloc[2] = {nullptr, nullptr};
+    size_t alloc_bytes = 0;
+    Weights w;
+    double* d_field = nullptr;
+    int64_t field_cap = 0;
+    double* d_partials = nullptr;  // mass partial sums
+    double* d_scalar = nullptr;    // misc device scalars
+    int* d_err = nullptr;          // sticky device error flag
+    double* d_stage = nullptr;     // set/get staging (device)
+    double* h_stage = nullptr;     // set/get staging (pinned host)
+    size_t stage_elems = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int device = 0;
+    // distribution
+    int rank = 0, world = 1;
+    void* comm = nullptr;  // ncclComm_t
+    bool own_comm = false;
+    // instrumentation
+    bool profile = false;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> ev_pairs;
+    std::vector<double> ev_bytes;
+    std::vector<int> ev_dim;
+    std::vector<cudaEvent_t> ev_pool;
+    double prof_ms[kMaxDim] = {}, prof_bytes[kMaxDim] = {};
+    int64_t prof_launches[kMaxDim] = {};
+    int64_t launches = 0;
+};
+
+// ---- kernel launchers (sldg_kernels.cu) -------------------------------------------------
+cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field, double shift,
+                           int64_t n_entries, Weights& w, int* d_err, cudaStream_t s);
+cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
+                         int64_t layer_begin, int64_t layer_end, cudaStream_t s, int* n_launched);
+cudaError_t launch_mass_partials(const Layout& lay, const Arrays& a, double* d_partials,
+                                 double* d_out, cudaStream_t s);
+cudaError_t launch_set(const Layout& lay, const Arrays& a, const double* d_src, int64_t first_cell,
+                       int64_t n_cells, cudaStream_t s);
+cudaError_t launch_get(const Layout& lay, const Arrays& a, double* d_dst, int64_t first_cell,
+                       int64_t n_cells, cudaStream_t s);
+cudaError_t launch_fill_random(const Layout& lay, const Arrays& a, uint64_t seed, cudaStream_t s);
+cudaError_t launch_fill_separable(const Layout& lay, const Arrays& a, int n_terms,
+                                  const double* d_tables, cudaStream_t s);
+cudaError_t launch_field_range(const double* d_field, int64_t n, double shift, int64_t* d_out2,
+                               cudaStream_t s);
+
+constexpr int kMassBlocks = 592;  // 4 x 148 SMs; fixed => deterministic reduction order
+
+}  // namespace sldg

@@ -1,0 +1,713 @@
+// sldg_kernels.cu -- sm_100a kernels of the mixed-precision SLDG step (arXiv:1603.07008).
+//
+// Hot path:
+//   build_weights   a1 shift decomposition + a2 weight build (A, B per field entry)
+//   sweep_d0        a3-a7 for the contiguous dim 0 (lane = target cell, neighbour source by
+//                   warp shuffle, every slot read from HBM once)
+//   sweep_strided   a3-a7 for dims >= 1 (lane = consecutive i_0 so every warp access is a
+//                   coalesced row segment; register sliding window of T targets along dim)
+// Auxiliary: mass reduction (a9), set/get conversion, synthetic fills.
+//
+// Arithmetic is fp64 throughout (reading R6): fp32 slots are promoted exactly on load and
+// rounded to nearest-even on store (__double2float_rn; no fast-math, no FTZ).
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "sldg_internal.h"
+
+namespace sldg {
+
+// ============================================================================================
+// Element access
+// ============================================================================================
+template <int PREC>
+__device__ __forceinline__ double ld_slot(const Arrays& a, const Layout& L, int q, int64_t layerp,
+                                          int64_t inner)
+{
+    if (PREC == SLDG_FP64) return __ldg(&a.s64[(layerp * L.K + q) * L.L + inner]);
+    if (q == 0) return __ldg(&a.mass[layerp * L.L + inner]);
+    return (double)__ldg(&a.pl[(layerp * (L.K - 1) + (q - 1)) * L.L + inner]);
+}
+
+template <int PREC>
+__device__ __forceinline__ void st_slot(const Arrays& a, const Layout& L, int q, int64_t layerp,
+                                        int64_t inner, double v)
+{
+    if (PREC == SLDG_FP64) {
+        __stcs(&a.s64[(layerp * L.K + q) * L.L + inner], v);
+    } else if (q == 0) {
+        __stcs(&a.mass[layerp * L.L + inner], v);
+    } else {
+        __stcs(&a.pl[(layerp * (L.K - 1) + (q - 1)) * L.L + inner], __double2float_rn(v));
+    }
+}
+
+// ============================================================================================
+// a1 + a2: shift decomposition and weight build, one thread per field entry.
+// A_jl = (2j+1)/2 int_{-1}^{2a-1} P_l(xi+2-2a) P_j(xi) dxi,  B_jl = (2j+1)/2 int_{2a-1}^{1}
+// P_l(xi-2a) P_j(xi) dxi (P:259-268 SS II-A), each by a k-point Gauss-Legendre rule
+// mapped to the sub-interval (exact for the degree <= 2k-2 integrand), mass row in closed
+// form (reading R3), alpha == 0 -> A = 0, B = I and the exact-copy flag (reading R4).
+// ============================================================================================
+__device__ void dev_legendre(int pmax, double x, double* P)
+{
+    P[0] = 1.0;
+    if (pmax > 0) P[1] = x;
+    for (int n = 2; n <= pmax; ++n) P[n] = ((2 * n - 1) * x * P[n - 1] - (n - 1) * P[n - 2]) / n;
+}
+
+// Gauss-Legendre nodes/weights on [-1,1] by Newton on P_n (roots symmetric; compute the
+// non-negative half and mirror).
+__device__ void dev_gauss(int n, double* x, double* w)
+{
+    const double kPi = 3.141592653589793238462643;
+    for (int i = 0; i < (n + 1) / 2; ++i) {
+        double z = cos(kPi * (i + 0.75) / (n + 0.5));
+        double pn = 0.0, dpn = 1.0;
+        for (int it = 0; it < 60; ++it) {
+            double p0 = 1.0, p1 = z;
+            for (int m = 2; m <= n; ++m) {
+                double p2 = ((2 * m - 1) * z * p1 - (m - 1) * p0) / m;
+                p0 = p1;
+                p1 = p2;
+            }
+            pn = (n == 1) ? z : p1;
+            double pm1 = (n == 1) ? 1.0 : p0;
+            dpn = n * (pm1 - z * pn) / (1.0 - z * z);
+            double dz = pn / dpn;
+            z -= dz;
+            if (fabs(dz) < 1e-17) break;
+        }
+        {  // derivative at the converged node
+            double p0 = 1.0, p1 = z;
+            for (int m = 2; m <= n; ++m) {
+                double p2 = ((2 * m - 1) * z * p1 - (m - 1) * p0) / m;
+                p0 = p1;
+                p1 = p2;
+            }
+            double pm1 = (n == 1) ? 1.0 : p0;
+            double pnn = (n == 1) ? z : p1;
+            dpn = n * (pm1 - z * pnn) / (1.0 - z * z);
+        }
+        double wi = 2.0 / ((1.0 - z * z) * dpn * dpn);
+        x[i] = -z;
+        w[i] = wi;
+        x[n - 1 - i] = z;
+        w[n - 1 - i] = wi;
+    }
+    if (n & 1) x[n / 2] = 0.0;
+}
+
+__global__ void build_weights_kernel(int k, int64_t nd, const double* __restrict__ field, double shift,
+                                     int64_t n_entries, int64_t* __restrict__ sh_raw,
+                                     int64_t* __restrict__ sh_mod, int* __restrict__ cpy,
+                                     double* __restrict__ ab, int* __restrict__ err)
+{
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_entries) return;
+    double nu = field ? field[e] : shift;
+    double* A = ab + e * 2 * k * k;
+    double* B = A + k * k;
+    int64_t is = 0;
+    double a = 0.0;
+    if (!(fabs(nu) < 4.611686018427387904e18)) {  // non-finite or |nu| >= 2^62
+        atomicExch(err, 1);
+    } else {
+        double fl = floor(nu);
+        a = nu - fl;
+        is = (int64_t)fl;
+        if (a >= 1.0) {  // tiny negative nu: alpha rounds to 1 (reading R2)
+            is += 1;
+            a = 0.0;
+        }
+    }
+    sh_raw[e] = is;
+    int64_t m = is % nd;
+    sh_mod[e] = m < 0 ? m + nd : m;
+    cpy[e] = (a == 0.0);
+    for (int j = 0; j < k * k; ++j) {
+        A[j] = 0.0;
+        B[j] = ((j / k) == (j % k)) ? 1.0 : 0.0;
+    }
+    if (a == 0.0) return;
+
+    double xg[kMaxK], wg[kMaxK], Pj[kMaxK + 2], Pl[kMaxK + 2];
+    dev_gauss(k, xg, wg);
+    for (int j = 0; j < k * k; ++j) {
+        A[j] = 0.0;
+        B[j] = 0.0;
+    }
+    for (int g = 0; g < k; ++g) {
+        // A: xi in [-1, 2a-1] -> xi = (a - 1) + a t ; integrand P_l(xi + 2 - 2a) P_j(xi)
+        double xi = (a - 1.0) + a * xg[g];
+        dev_legendre(k - 1, xi, Pj);
+        dev_legendre(k - 1, xi + 2.0 - 2.0 * a, Pl);
+        for (int j = 0; j < k; ++j)
+            for (int l = 0; l < k; ++l) A[j * k + l] += wg[g] * (Pj[j] * Pl[l]);
+        // B: xi in [2a-1, 1] -> xi = a + (1 - a) t ; integrand P_l(xi - 2a) P_j(xi)
+        xi = a + (1.0 - a) * xg[g];
+        dev_legendre(k - 1, xi, Pj);
+        dev_legendre(k - 1, xi - 2.0 * a, Pl);
+        for (int j = 0; j < k; ++j)
+            for (int l = 0; l < k; ++l) B[j * k + l] += wg[g] * (Pj[j] * Pl[l]);
+    }
+    for (int j = 0; j < k; ++j) {
+        double sa = 0.5 * (2 * j + 1) * a, sb = 0.5 * (2 * j + 1) * (1.0 - a);
+        for (int l = 0; l < k; ++l) {
+            A[j * k + l] *= sa;
+            B[j * k + l] *= sb;
+        }
+    }
+    // mass row, closed form (reading R3): int_x^1 P_l = -(P_{l+1}(x) - P_{l-1}(x))/(2l+1)
+    {
+        double P[kMaxK + 2];
+        dev_legendre(k, 1.0 - 2.0 * a, P);
+        for (int l = 1; l < k; ++l) {
+            double v = -(P[l + 1] - P[l - 1]) / (2.0 * (2 * l + 1));
+            A[l] = v;
+            B[l] = -v;
+        }
+        if (a <= 0.5) {
+            B[0] = 1.0 - a;
+            A[0] = 1.0 - B[0];
+        } else {
+            A[0] = a;
+            B[0] = 1.0 - a;
+        }
+    }
+}
+
+cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field, double shift,
+                           int64_t n_entries, Weights& w, int* d_err, cudaStream_t s)
+{
+    int threads = 128;
+    int64_t blocks = (n_entries + threads - 1) / threads;
+    build_weights_kernel<<<(unsigned)blocks, threads, 0, s>>>(lay.k, nd, d_field, shift, n_entries,
+                                                              w.shift, w.smod, w.copy, w.ab, d_err);
+    return cudaGetLastError();
+}
+
+// ============================================================================================
+// Field index of a line from its perpendicular indices.
+// ============================================================================================
+__device__ __forceinline__ int64_t field_index(const Sweep& sw, const int64_t* idx, int D)
+{
+    int64_t f = 0;
+    if (sw.fmask) {
+#pragma unroll
+        for (int e = 0; e < kMaxDim; ++e)
+            if (e < D) f += idx[e] * sw.fstride[e];
+    }
+    return f;
+}
+
+// ============================================================================================
+// a3-a7 along the contiguous dim 0.  One thread = one target cell (all k^{D-1} coupled
+// groups); lanes hold consecutive cells of a line so the B-source row of the warp is one
+// contiguous segment, and each lane's A-source (i - i* - 1) is its left neighbour's B-source
+// (i - 1 - i*), received by __shfl_up (neighbour reuse).  Lanes whose neighbour
+// is not in the warp/line load it themselves.
+// ============================================================================================
+template <int KK, int PREC>
+__global__ void __launch_bounds__(256) sweep_d0_kernel(Layout lay, Sweep sw, Arrays src, Arrays dst,
+                                                       int64_t layer_begin, int64_t layer_end)
+{
+    const int64_t L = lay.L;
+    const int64_t n0 = lay.n[0];
+    const int64_t total = (layer_end - layer_begin) * L;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (total == 0) return;
+    const bool active = t < total;
+    if (!active) t = total - 1;  // inactive lanes still take part in the shuffles
+    const int64_t layer = layer_begin + t / L;
+    const int64_t inner = t - (t / L) * L;
+    const int64_t i0 = inner % n0;
+
+    int64_t idx[kMaxDim];
+    {
+        int64_t rem = inner;
+#pragma unroll
+        for (int e = 0; e < kMaxDim; ++e) {
+            if (e < lay.D - 1 || (lay.D == 1 && e == 0)) {
+                idx[e] = rem % lay.n[e];
+                rem /= lay.n[e];
+            } else {
+                idx[e] = 0;
+            }
+        }
+        if (lay.D >= 2) idx[lay.D - 1] = lay.first_layer + layer;
+    }
+    const int64_t f = field_index(sw, idx, lay.D);
+    const int64_t s = __ldg(&sw.smod[f]);
+    const int cp = __ldg(&sw.copy[f]);
+    const double* __restrict__ w = sw.ab + f * (2 * KK * KK);
+
+    int64_t iB = i0 - s;
+    if (iB < 0) iB += n0;
+    int64_t iA = iB - 1;
+    if (iA < 0) iA += n0;
+    const int64_t base = inner - i0;
+    const int lane = threadIdx.x & 31;
+    const bool from_nbr = (lane > 0) && (i0 > 0);
+    const int64_t layerp = lay.pad + layer;
+    const int G = lay.K / KK;
+
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+        double a[KK], b[KK];
+#pragma unroll
+        for (int j = 0; j < KK; ++j) b[j] = ld_slot<PREC>(src, lay, g * KK + j, layerp, base + iB);
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            double v = __shfl_up_sync(0xffffffffu, b[j], 1);
+            if (!from_nbr) v = ld_slot<PREC>(src, lay, g * KK + j, layerp, base + iA);
+            a[j] = v;
+        }
+        if (active) {
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                double o;
+                if (cp) {
+                    o = b[j];
+                } else {
+                    o = 0.0;
+#pragma unroll
+                    for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[j * KK + l]), a[l], o);
+#pragma unroll
+                    for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[KK * KK + j * KK + l]), b[l], o);
+                }
+                st_slot<PREC>(dst, lay, g * KK + j, layerp, inner, o);
+            }
+        }
+    }
+}
+
+// ============================================================================================
+// a3-a7 along a strided dim d >= 1.  One thread = (i_0, other perpendicular indices,
+// segment of T consecutive targets along d, one coupled group).  Lanes run along i_0, so
+// every load/store instruction of a warp touches one contiguous row segment (coalesced) even
+// when the line shifts differ per lane (per-lane CFL fields).  Along the segment each source
+// row is loaded once and reused as the next target's A-source (register sliding window).
+// ============================================================================================
+template <int KK, int PREC, int T>
+__global__ void __launch_bounds__(256) sweep_strided_kernel(Layout lay, Sweep sw, Arrays src, Arrays dst,
+                                                            int64_t layer_begin, int64_t layer_end)
+{
+    const int D = lay.D;
+    const int d = sw.dim;
+    const bool outer = (d == D - 1);
+    const int64_t nlay = layer_end - layer_begin;
+    const int64_t nline = outer ? nlay : sw.nd;  // targets along the line handled here
+    const int64_t nseg = (nline + T - 1) / T;
+    int G = 1;
+    for (int e = 0; e < D - 1; ++e) G *= KK;
+
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t idx[kMaxDim];
+    int64_t rem = t;
+    idx[0] = rem % lay.n[0];
+    rem /= lay.n[0];
+#pragma unroll
+    for (int e = 1; e < kMaxDim; ++e) {
+        idx[e] = 0;
+        if (e < D - 1 && e != d) {
+            idx[e] = rem % lay.n[e];
+            rem /= lay.n[e];
+        }
+    }
+    int64_t layer = 0;
+    if (!outer) {
+        layer = layer_begin + rem % nlay;
+        rem /= nlay;
+        idx[D - 1] = lay.first_layer + layer;
+    }
+    const int64_t seg = rem % nseg;
+    rem /= nseg;
+    const int64_t g = rem;
+    if (g >= G || nlay == 0) return;
+
+    // coupled group g -> base slot (digits of g over dims e != d, ascending)
+    int qbase = 0, kd = 1;
+    {
+        int gg = (int)g, kp = 1;
+        for (int e = 0; e < D; ++e) {
+            if (e == d) {
+                kd = kp;
+            } else {
+                qbase += (gg % KK) * kp;
+                gg /= KK;
+            }
+            kp *= KK;
+        }
+    }
+
+    idx[d] = 0;
+    const int64_t f = field_index(sw, idx, D);
+    const int cp = __ldg(&sw.copy[f]);
+    const double* __restrict__ w = sw.ab + f * (2 * KK * KK);
+
+    // inner offset of the line start (i_d = 0) and stride along the line
+    int64_t inner0 = 0;
+    for (int e = 0; e < D - 1; ++e) inner0 += idx[e] * lay.S[e];
+    const int64_t step = outer ? 0 : lay.S[d];
+
+    // first target (line coordinate) and source positions
+    const int64_t t0 = seg * T;  // local target index along the line
+    int64_t nt = nline - t0;
+    if (nt > T) nt = T;
+
+    // source line coordinate of the A-source of target t0:  (tg - i* - 1)
+    int64_t sp;  // source position in "line coordinates" (layer index for outer, i_d otherwise)
+    if (outer) {
+        const int64_t tg = lay.first_layer + layer_begin + t0;  // global target layer
+        if (sw.wrap) {
+            int64_t s = __ldg(&sw.smod[f]);
+            sp = tg - s - 1;
+            sp %= sw.nd;
+            if (sp < 0) sp += sw.nd;
+        } else {
+            sp = tg - __ldg(&sw.shift[f]) - 1 - lay.first_layer;  // local layer (may be halo)
+        }
+    } else {
+        int64_t s = __ldg(&sw.smod[f]);
+        sp = t0 - s - 1;
+        if (sp < 0) sp += sw.nd;
+    }
+
+    double v[T + 1][KK];
+#pragma unroll
+    for (int p = 0; p <= T; ++p) {
+        if (p <= nt) {
+            int64_t lp, in;
+            if (outer) {
+                lp = lay.pad + sp;
+                in = inner0;
+            } else {
+                lp = lay.pad + layer;
+                in = inner0 + sp * step;
+            }
+#pragma unroll
+            for (int j = 0; j < KK; ++j) v[p][j] = ld_slot<PREC>(src, lay, qbase + j * kd, lp, in);
+        }
+        ++sp;
+        if (sw.wrap && sp == sw.nd) sp = 0;
+    }
+#pragma unroll
+    for (int p = 1; p <= T; ++p) {
+        if (p <= nt) {
+            const int64_t tl = t0 + p - 1;
+            int64_t lp, in;
+            if (outer) {
+                lp = lay.pad + layer_begin + tl;
+                in = inner0;
+            } else {
+                lp = lay.pad + layer;
+                in = inner0 + tl * step;
+            }
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                double o;
+                if (cp) {
+                    o = v[p][j];
+                } else {
+                    o = 0.0;
+#pragma unroll
+                    for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[j * KK + l]), v[p - 1][l], o);
+#pragma unroll
+                    for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[KK * KK + j * KK + l]), v[p][l], o);
+                }
+                st_slot<PREC>(dst, lay, qbase + j * kd, lp, in, o);
+            }
+        }
+    }
+}
+
+template <int KK, int PREC>
+static cudaError_t launch_sweep_k(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
+                                  int64_t lb, int64_t le, cudaStream_t s)
+{
+    const int threads = 256;
+    if (sw.dim == 0) {
+        int64_t total = (le - lb) * lay.L;
+        if (total == 0) return cudaSuccess;
+        int64_t blocks = (total + threads - 1) / threads;
+        sweep_d0_kernel<KK, PREC><<<(unsigned)blocks, threads, 0, s>>>(lay, sw, src, dst, lb, le);
+    } else {
+        constexpr int T = (KK <= 2) ? 16 : (KK <= 4 ? 8 : 4);
+        const bool outer = (sw.dim == lay.D - 1);
+        int64_t nline = outer ? (le - lb) : sw.nd;
+        int64_t nseg = (nline + T - 1) / T;
+        int64_t perp = 1;  // perpendicular lines (excluding the layer dim)
+        for (int e = 0; e < lay.D - 1; ++e)
+            if (e != sw.dim) perp *= lay.n[e];
+        int64_t G = 1;
+        for (int e = 0; e < lay.D - 1; ++e) G *= KK;
+        int64_t total = perp * (outer ? 1 : (le - lb)) * nseg * G;
+        if (total == 0) return cudaSuccess;
+        int64_t blocks = (total + threads - 1) / threads;
+        sweep_strided_kernel<KK, PREC, T><<<(unsigned)blocks, threads, 0, s>>>(lay, sw, src, dst, lb, le);
+    }
+    return cudaGetLastError();
+}
+
+template <int PREC>
+static cudaError_t launch_sweep_p(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
+                                  int64_t lb, int64_t le, cudaStream_t s)
+{
+    switch (lay.k) {
+        case 1: return launch_sweep_k<1, PREC>(lay, sw, src, dst, lb, le, s);
+        case 2: return launch_sweep_k<2, PREC>(lay, sw, src, dst, lb, le, s);
+        case 3: return launch_sweep_k<3, PREC>(lay, sw, src, dst, lb, le, s);
+        case 4: return launch_sweep_k<4, PREC>(lay, sw, src, dst, lb, le, s);
+        case 5: return launch_sweep_k<5, PREC>(lay, sw, src, dst, lb, le, s);
+        case 6: return launch_sweep_k<6, PREC>(lay, sw, src, dst, lb, le, s);
+        case 7: return launch_sweep_k<7, PREC>(lay, sw, src, dst, lb, le, s);
+        case 8: return launch_sweep_k<8, PREC>(lay, sw, src, dst, lb, le, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
+                         int64_t layer_begin, int64_t layer_end, cudaStream_t s, int* n_launched)
+{
+    *n_launched = (layer_end > layer_begin) ? 1 : 0;
+    if (lay.prec == SLDG_FP64) return launch_sweep_p<SLDG_FP64>(lay, sw, src, dst, layer_begin, layer_end, s);
+    return launch_sweep_p<SLDG_MIXED>(lay, sw, src, dst, layer_begin, layer_end, s);
+}
+
+// ============================================================================================
+// a9: mass = sum of slot 0 over local cells, fixed-order two-pass reduction with Neumaier
+// compensation per thread (deterministic for a fixed grid: kMassBlocks x 256 threads).
+// ============================================================================================
+__device__ __forceinline__ void neumaier_add(double& s, double& c, double x)
+{
+    double t = s + x;
+    if (fabs(s) >= fabs(x)) c += (s - t) + x;
+    else c += (x - t) + s;
+    s = t;
+}
+
+__global__ void __launch_bounds__(256) mass_partials_kernel(Layout lay, Arrays a, double* __restrict__ partials)
+{
+    __shared__ double sh[256];
+    double s = 0.0, c = 0.0;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < lay.cells; e += stride) {
+        int64_t layer = e / lay.L, inner = e - layer * lay.L;
+        double x = (lay.prec == SLDG_FP64) ? a.s64[((lay.pad + layer) * lay.K) * lay.L + inner]
+                                           : a.mass[(lay.pad + layer) * lay.L + inner];
+        neumaier_add(s, c, x);
+    }
+    sh[threadIdx.x] = s + c;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+__global__ void __launch_bounds__(1024) mass_final_kernel(const double* __restrict__ partials, int n,
+                                                          double* __restrict__ out)
+{
+    __shared__ double sh[1024];
+    sh[threadIdx.x] = threadIdx.x < n ? partials[threadIdx.x] : 0.0;
+    __syncthreads();
+    for (int off = 512; off > 0; off >>= 1) {
+        if (threadIdx.x < off) sh[threadIdx.x] += sh[threadIdx.x + off];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *out = sh[0];
+}
+
+cudaError_t launch_mass_partials(const Layout& lay, const Arrays& a, double* d_partials, double* d_out,
+                                 cudaStream_t s)
+{
+    mass_partials_kernel<<<kMassBlocks, 256, 0, s>>>(lay, a, d_partials);
+    mass_final_kernel<<<1, 1024, 0, s>>>(d_partials, kMassBlocks, d_out);
+    return cudaGetLastError();
+}
+
+// ============================================================================================
+// set / get: host AoS fp64 [cell][q] chunk <-> device split layout.  RNE narrowing.
+// ============================================================================================
+__global__ void set_kernel(Layout lay, Arrays a, const double* __restrict__ srcv, int64_t first_cell,
+                           int64_t n_elems)
+{
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    int64_t cell = first_cell + e / lay.K;
+    int q = (int)(e % lay.K);
+    int64_t layer = cell / lay.L, inner = cell - layer * lay.L;
+    double v = srcv[e];
+    int64_t lp = lay.pad + layer;
+    if (lay.prec == SLDG_FP64) a.s64[(lp * lay.K + q) * lay.L + inner] = v;
+    else if (q == 0) a.mass[lp * lay.L + inner] = v;
+    else a.pl[(lp * (lay.K - 1) + (q - 1)) * lay.L + inner] = __double2float_rn(v);
+}
+
+__global__ void get_kernel(Layout lay, Arrays a, double* __restrict__ dstv, int64_t first_cell, int64_t n_elems)
+{
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= n_elems) return;
+    int64_t cell = first_cell + e / lay.K;
+    int q = (int)(e % lay.K);
+    int64_t layer = cell / lay.L, inner = cell - layer * lay.L;
+    int64_t lp = lay.pad + layer;
+    double v;
+    if (lay.prec == SLDG_FP64) v = a.s64[(lp * lay.K + q) * lay.L + inner];
+    else if (q == 0) v = a.mass[lp * lay.L + inner];
+    else v = (double)a.pl[(lp * (lay.K - 1) + (q - 1)) * lay.L + inner];
+    dstv[e] = v;
+}
+
+cudaError_t launch_set(const Layout& lay, const Arrays& a, const double* d_src, int64_t first_cell,
+                       int64_t n_cells, cudaStream_t s)
+{
+    int64_t n = n_cells * lay.K;
+    if (n == 0) return cudaSuccess;
+    set_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lay, a, d_src, first_cell, n);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_get(const Layout& lay, const Arrays& a, double* d_dst, int64_t first_cell, int64_t n_cells,
+                       cudaStream_t s)
+{
+    int64_t n = n_cells * lay.K;
+    if (n == 0) return cudaSuccess;
+    get_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lay, a, d_dst, first_cell, n);
+    return cudaGetLastError();
+}
+
+// ============================================================================================
+// Synthetic fills (inputs, not the method).
+// ============================================================================================
+__device__ __forceinline__ uint64_t splitmix64_dev(uint64_t z)
+{
+    z += 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+__global__ void fill_random_kernel(Layout lay, Arrays a, uint64_t seed)
+{
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= lay.cells * lay.K) return;
+    int64_t cell = e / lay.K;
+    int q = (int)(e - cell * lay.K);
+    int64_t gcell = lay.first_layer * lay.L + cell;
+    uint64_t z = seed * (1ull << 40) + (uint64_t)gcell * (uint64_t)lay.K + (uint64_t)q;
+    uint64_t hsh = splitmix64_dev(z);
+    double u = (double)(hsh >> 11) * 0x1.0p-53;
+    double r = 2.0 * u - 1.0;
+    double v;
+    if (q == 0) {
+        v = __dadd_rn(1.0, __dmul_rn(0.5, r));
+    } else {
+        int deg = 0, qq = q;
+        for (int dd = 0; dd < lay.D; ++dd) {
+            deg += qq % lay.k;
+            qq /= lay.k;
+        }
+        uint64_t p = 1;
+        for (int i = 0; i < deg; ++i) p *= (uint64_t)lay.n[0];
+        v = __ddiv_rn(r, __ull2double_rn(p));
+    }
+    int64_t layer = cell / lay.L, inner = cell - layer * lay.L;
+    int64_t lp = lay.pad + layer;
+    if (lay.prec == SLDG_FP64) a.s64[(lp * lay.K + q) * lay.L + inner] = v;
+    else if (q == 0) a.mass[lp * lay.L + inner] = v;
+    else a.pl[(lp * (lay.K - 1) + (q - 1)) * lay.L + inner] = __double2float_rn(v);
+}
+
+cudaError_t launch_fill_random(const Layout& lay, const Arrays& a, uint64_t seed, cudaStream_t s)
+{
+    int64_t n = lay.cells * lay.K;
+    if (n == 0) return cudaSuccess;
+    fill_random_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lay, a, seed);
+    return cudaGetLastError();
+}
+
+__global__ void fill_separable_kernel(Layout lay, Arrays a, int n_terms, const double* __restrict__ tab)
+{
+    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (e >= lay.cells * lay.K) return;
+    int64_t cell = e / lay.K;
+    int q = (int)(e - cell * lay.K);
+    int64_t layer = cell / lay.L, inner = cell - layer * lay.L;
+    int64_t idx[kMaxDim];
+    int m[kMaxDim];
+    int64_t rem = inner;
+    int qq = q;
+    int64_t off[kMaxDim], term_stride = 0;
+    for (int d = 0; d < lay.D; ++d) {
+        off[d] = term_stride;
+        term_stride += lay.n[d] * lay.k;
+        m[d] = qq % lay.k;
+        qq /= lay.k;
+        if (d < lay.D - 1 || lay.D == 1) {
+            idx[d] = rem % lay.n[d];
+            rem /= lay.n[d];
+        }
+    }
+    if (lay.D >= 2) idx[lay.D - 1] = lay.first_layer + layer;
+    double v = 0.0;
+    for (int t = 0; t < n_terms; ++t) {
+        double p = 1.0;
+        for (int d = 0; d < lay.D; ++d) p *= tab[t * term_stride + off[d] + idx[d] * lay.k + m[d]];
+        v += p;
+    }
+    int64_t lp = lay.pad + layer;
+    if (lay.prec == SLDG_FP64) a.s64[(lp * lay.K + q) * lay.L + inner] = v;
+    else if (q == 0) a.mass[lp * lay.L + inner] = v;
+    else a.pl[(lp * (lay.K - 1) + (q - 1)) * lay.L + inner] = __double2float_rn(v);
+}
+
+cudaError_t launch_fill_separable(const Layout& lay, const Arrays& a, int n_terms, const double* d_tables,
+                                  cudaStream_t s)
+{
+    int64_t n = lay.cells * lay.K;
+    if (n == 0) return cudaSuccess;
+    fill_separable_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lay, a, n_terms, d_tables);
+    return cudaGetLastError();
+}
+
+// min / max of floor(nu) over a device field (halo planning for sharded sweeps)
+__global__ void field_range_kernel(const double* __restrict__ field, int64_t n, double shift, int64_t* out)
+{
+    __shared__ int64_t smin[256], smax[256];
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) {
+        double nu = field ? field[e] : shift;
+        if (!(fabs(nu) < 4.611686018427387904e18)) continue;
+        double fl = floor(nu);
+        int64_t is = (int64_t)fl;
+        if (nu - fl >= 1.0) is += 1;
+        lo = is < lo ? is : lo;
+        hi = is > hi ? is : hi;
+    }
+    smin[threadIdx.x] = lo;
+    smax[threadIdx.x] = hi;
+    __syncthreads();
+    for (int off = 128; off > 0; off >>= 1) {
+        if (threadIdx.x < off) {
+            smin[threadIdx.x] = min(smin[threadIdx.x], smin[threadIdx.x + off]);
+            smax[threadIdx.x] = max(smax[threadIdx.x], smax[threadIdx.x + off]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = smin[0];
+        out[1] = smax[0];
+    }
+}
+
+cudaError_t launch_field_range(const double* d_field, int64_t n, double shift, int64_t* d_out2, cudaStream_t s)
+{
+    field_range_kernel<<<1, 256, 0, s>>>(d_field, n, shift, d_out2);
+    return cudaGetLastError();
+}
+
+}  // namespace sldg

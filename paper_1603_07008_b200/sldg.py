@@ -1,0 +1,236 @@
+"""Thin ctypes binding of include/sldg.h (argument marshalling only).
+
+Every step of the SLDG path runs in libsldg.so (sm_100a CUDA kernels); this module only
+converts Python/numpy arguments to C and raises on non-OK status.  There is no CPU fallback:
+if the shared library is missing or a call fails, an exception is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsldg.so")
+
+SLDG_OK, SLDG_EINVAL, SLDG_ENOMEM, SLDG_ECUDA, SLDG_ENCCL, SLDG_ENOTSUP = range(6)
+SLDG_MIXED, SLDG_FP64 = 0, 1
+MAX_DIM = 6
+STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "ENOTSUP"}
+
+# every symbol include/sldg.h declares
+EXPORTS = [
+    "sldg_create", "sldg_destroy", "sldg_set_coeffs", "sldg_get_coeffs", "sldg_advect",
+    "sldg_advect_device", "sldg_mass", "sldg_shard_info", "sldg_sync", "sldg_set_stream",
+    "sldg_get_stream", "sldg_memory_bytes", "sldg_last_error", "sldg_fill_random",
+    "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
+    "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_layer_owner",
+]
+
+
+class SldgError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+class GridDesc(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int), ("cells", ctypes.c_int64 * MAX_DIM)]
+
+
+class Domain(ctypes.Structure):
+    _fields_ = [("lo", ctypes.c_double * MAX_DIM), ("hi", ctypes.c_double * MAX_DIM)]
+
+
+class Dist(ctypes.Structure):
+    _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
+                ("nccl_comm", ctypes.c_void_p), ("max_halo", ctypes.c_int)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libsldg.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing; run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    i64, u32, dp, vp = ctypes.c_int64, ctypes.c_uint32, ctypes.POINTER(ctypes.c_double), ctypes.c_void_p
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    sig = {
+        "sldg_create": [ctypes.POINTER(GridDesc), ctypes.c_int, ctypes.POINTER(Domain), ctypes.c_int,
+                        ctypes.POINTER(Dist), ctypes.POINTER(vp)],
+        "sldg_destroy": [vp],
+        "sldg_set_coeffs": [vp, dp, i64, i64],
+        "sldg_get_coeffs": [vp, dp, i64, i64],
+        "sldg_advect": [vp, ctypes.c_int, ctypes.c_double, dp, u32],
+        "sldg_advect_device": [vp, ctypes.c_int, ctypes.c_double, vp, u32],
+        "sldg_mass": [vp, dp],
+        "sldg_shard_info": [vp, i64p, i64p],
+        "sldg_sync": [vp],
+        "sldg_set_stream": [vp, vp],
+        "sldg_get_stream": [vp, ctypes.POINTER(vp)],
+        "sldg_fill_random": [vp, ctypes.c_uint64],
+        "sldg_fill_separable": [vp, ctypes.c_int, dp],
+        "sldg_profile": [vp, ctypes.c_int],
+        "sldg_kernel_time": [vp, ctypes.c_int, dp, i64p, dp, ctypes.c_int],
+        "sldg_nccl_unique_id": [vp],
+        "sldg_halo_widths": [i64, i64, i64p, i64p],
+        "sldg_layer_owner": [i64, ctypes.c_int, i64, ctypes.POINTER(ctypes.c_int), i64p],
+    }
+    for name, args in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = ctypes.c_int
+    L.sldg_memory_bytes.argtypes = [vp]
+    L.sldg_memory_bytes.restype = ctypes.c_size_t
+    L.sldg_last_error.argtypes = []
+    L.sldg_last_error.restype = ctypes.c_char_p
+    L.sldg_launch_count.argtypes = [vp]
+    L.sldg_launch_count.restype = ctypes.c_int64
+    _lib = L
+    return L
+
+
+def _check(st: int):
+    if st != SLDG_OK:
+        raise SldgError(st, lib().sldg_last_error().decode(errors="replace"))
+
+
+def _dp(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().sldg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def halo_widths(imin: int, imax: int):
+    a, b = ctypes.c_int64(), ctypes.c_int64()
+    _check(lib().sldg_halo_widths(imin, imax, ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def layer_owner(n: int, world: int, layer: int):
+    o, loc = ctypes.c_int(), ctypes.c_int64()
+    _check(lib().sldg_layer_owner(n, world, layer, ctypes.byref(o), ctypes.byref(loc)))
+    return o.value, loc.value
+
+
+class Grid:
+    """Owns one sldg_grid handle.  Method names follow the C ABI (sldg_<name>)."""
+
+    def __init__(self, cells, k: int, lo=None, hi=None, precision: str = "mixed",
+                 rank: int = 0, world: int = 1, unique_id: bytes | None = None, max_halo: int = 0):
+        cells = [int(c) for c in cells]
+        self.D = len(cells)
+        self.cells = cells
+        self.k = int(k)
+        self.K = self.k ** self.D
+        self.precision = precision
+        lo = list(lo) if lo is not None else [0.0] * self.D
+        hi = list(hi) if hi is not None else [1.0] * self.D
+        gd = GridDesc(self.D, (ctypes.c_int64 * MAX_DIM)(*(cells + [1] * (MAX_DIM - self.D))))
+        dom = Domain((ctypes.c_double * MAX_DIM)(*(lo + [0.0] * (MAX_DIM - self.D))),
+                     (ctypes.c_double * MAX_DIM)(*(hi + [1.0] * (MAX_DIM - self.D))))
+        prec = {"mixed": SLDG_MIXED, "fp64": SLDG_FP64}[precision]
+        dist_p = None
+        self._uid = None
+        if world > 1:
+            self._uid = ctypes.create_string_buffer(unique_id, 128)
+            dist = Dist(rank, world, ctypes.cast(self._uid, ctypes.c_void_p), None, max_halo)
+            dist_p = ctypes.byref(dist)
+        h = ctypes.c_void_p()
+        _check(lib().sldg_create(ctypes.byref(gd), self.k, ctypes.byref(dom), prec, dist_p, ctypes.byref(h)))
+        self.h = h
+        fl, nl = ctypes.c_int64(), ctypes.c_int64()
+        _check(lib().sldg_shard_info(self.h, ctypes.byref(fl), ctypes.byref(nl)))
+        self.first_layer, self.n_layers = fl.value, nl.value
+        per_layer = 1
+        for c in cells[:-1] if self.D > 1 else []:
+            per_layer *= c
+        self.local_cells = (nl.value * per_layer) if self.D > 1 else cells[0]
+
+    # -- lifecycle
+    def destroy(self):
+        if getattr(self, "h", None):
+            lib().sldg_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    # -- data
+    def set_coeffs(self, c: np.ndarray, first_cell: int = 0):
+        c = np.ascontiguousarray(c, dtype=np.float64)
+        n = c.size // self.K
+        _check(lib().sldg_set_coeffs(self.h, _dp(c), int(first_cell), n))
+
+    def get_coeffs(self, first_cell: int = 0, n_cells: int | None = None) -> np.ndarray:
+        if n_cells is None:
+            n_cells = self.local_cells - first_cell
+        out = np.empty((n_cells, self.K), dtype=np.float64)
+        _check(lib().sldg_get_coeffs(self.h, _dp(out), int(first_cell), int(n_cells)))
+        return out
+
+    def advect(self, dim: int, shift: float = 0.0, field=None, field_mask: int = 0):
+        if field is None:
+            _check(lib().sldg_advect(self.h, int(dim), float(shift), None, ctypes.c_uint32(field_mask)))
+        else:
+            f = np.ascontiguousarray(field, dtype=np.float64)
+            _check(lib().sldg_advect(self.h, int(dim), float(shift), _dp(f), ctypes.c_uint32(field_mask)))
+
+    def advect_device(self, dim: int, d_field_ptr: int, field_mask: int, shift: float = 0.0):
+        _check(lib().sldg_advect_device(self.h, int(dim), float(shift), ctypes.c_void_p(d_field_ptr),
+                                        ctypes.c_uint32(field_mask)))
+
+    def mass(self) -> float:
+        m = ctypes.c_double()
+        _check(lib().sldg_mass(self.h, ctypes.byref(m)))
+        return m.value
+
+    def sync(self):
+        _check(lib().sldg_sync(self.h))
+
+    def fill_random(self, seed: int):
+        _check(lib().sldg_fill_random(self.h, ctypes.c_uint64(seed)))
+
+    def fill_separable(self, terms):
+        """terms: list (per term) of lists (per dim) of [n_d, k] tables (GLOBAL n_d)."""
+        flat = np.concatenate([np.ascontiguousarray(t, dtype=np.float64).reshape(-1)
+                               for term in terms for t in term])
+        _check(lib().sldg_fill_separable(self.h, len(terms), _dp(flat)))
+
+    def memory_bytes(self) -> int:
+        return int(lib().sldg_memory_bytes(self.h))
+
+    # -- streams / instrumentation
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        _check(lib().sldg_get_stream(self.h, ctypes.byref(s)))
+        return s.value or 0
+
+    def set_stream(self, stream_ptr: int | None):
+        _check(lib().sldg_set_stream(self.h, ctypes.c_void_p(stream_ptr or 0)))
+
+    def profile(self, enable: bool):
+        _check(lib().sldg_profile(self.h, int(bool(enable))))
+
+    def kernel_time(self, dim: int = -1, reset: bool = False):
+        """(ms, launches, algorithmic bytes) of the sweep kernels along dim (-1: all)."""
+        ms, n, b = ctypes.c_double(), ctypes.c_int64(), ctypes.c_double()
+        _check(lib().sldg_kernel_time(self.h, int(dim), ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b),
+                                      int(reset)))
+        return ms.value, n.value, b.value
+
+    def launch_count(self) -> int:
+        return int(lib().sldg_launch_count(self.h))

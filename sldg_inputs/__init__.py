@@ -80,7 +80,8 @@ def random_coeffs(dims, k: int, seed: int, first_cell: int = 0, n_cells: int | N
 # ---------------------------------------------------------------------------------------
 # Landau-type initial value (SURVEY 8(d)), as separable 1D projections.
 # ---------------------------------------------------------------------------------------
-def _project_1d_np(f, n: int, lo: float, hi: float, k: int, quad_n: int = 10) -> np.ndarray:
+def project_1d(f, n: int, lo: float, hi: float, k: int, quad_n: int = 10) -> np.ndarray:
+    """[n, k] per-cell Legendre coefficients of f (numpy Gauss rule; input generation only)."""
     xq, wq = np.polynomial.legendre.leggauss(max(quad_n, k))
     V = np.polynomial.legendre.legvander(xq, k - 1)  # [quad, j]
     h = (hi - lo) / n
@@ -102,12 +103,12 @@ def landau_terms(dims, k: int, kinds, lo, hi, eps: float = 0.01, kappa: float = 
     base = []
     for d in range(D):
         f = g if kinds[d] == "v" else one
-        base.append(_project_1d_np(f, dims[d], lo[d], hi[d], k))
+        base.append(project_1d(f, dims[d], lo[d], hi[d], k))
     terms = [base]
     for d in range(D):
         if kinds[d] == "x":
             t = list(base)
-            t[d] = _project_1d_np(cosk, dims[d], lo[d], hi[d], k)
+            t[d] = project_1d(cosk, dims[d], lo[d], hi[d], k)
             terms.append(t)
     return terms
 

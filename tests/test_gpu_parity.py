@@ -1,0 +1,367 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on identical seeded
+inputs.  Tolerances (BASELINE.json north_star): fp64 mass slot |d| <= 1e-13 *
+max|c0| per array; fp32 slots |d| <= 8 ulp_fp32(max|plane|) per plane; fp64 variant 1e-13 *
+max|plane| per plane; integer shifts bit-exact; mass 1e-13 relative.
+"""
+import itertools
+
+import numpy as np
+import pytest
+
+import oracle
+import sldg_inputs
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+
+
+def _Grid(*a, **kw):
+    from paper_1603_07008_b200 import Grid
+    return Grid(*a, **kw)
+
+
+def assert_parity(got, ref, K, precision, tag=""):
+    got = np.asarray(got).reshape(-1, K)
+    ref = np.asarray(ref).reshape(-1, K)
+    for q in range(K):
+        m = np.max(np.abs(ref[:, q]))
+        d = np.max(np.abs(got[:, q] - ref[:, q]))
+        if precision == "fp64" or q == 0:
+            tol = 1e-13 * m
+        else:
+            tol = 8.0 * float(np.spacing(np.float32(m)))
+        assert d <= tol, f"{tag} slot {q}: |d|={d:.3e} > tol={tol:.3e} (max {m:.3e})"
+
+
+def n_double(precision, K):
+    return 1 if precision == "mixed" else K
+
+
+def oracle_input(c, K, precision):
+    return oracle.round_layout(c, K, n_double(precision, K))
+
+
+# ------------------------------------------------------------------------------ single sweeps
+CASES = [
+    # dims, k
+    ([64], 4),
+    ([100], 3),
+    ([1000], 1),
+    ([5], 6),
+    ([256, 64], 2),
+    ([100, 37], 4),
+    ([31, 33], 5),
+    ([48, 40], 6),
+    ([33, 7, 10], 3),
+    ([16, 6, 5, 9], 2),
+    ([8, 4, 6, 5], 3),
+    ([40, 3, 1, 7], 2),
+    ([12, 5, 4, 3, 2], 2),
+]
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+@pytest.mark.parametrize("dims,k", CASES)
+def test_single_sweeps_all_dims(dims, k, precision):
+    """Every dim, constant shifts of both signs and |nu| > n, and per-line fields over the
+    other dims (including per-lane fields on strided sweeps)."""
+    D, K = len(dims), k ** len(dims)
+    rng = np.random.default_rng(abs(hash((tuple(dims), k))) % 2**32)
+    c = sldg_inputs.random_coeffs(dims, k, 1603)
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision)
+    for dim in range(D):
+        others = [e for e in range(D) if e != dim]
+        variants = [("const", 2.37, None, 0), ("neg", -0.63 - dims[dim], None, 0)]
+        if others:
+            mask = 0
+            for e in others[: 2]:
+                mask |= 1 << e
+            nf = int(np.prod([dims[e] for e in range(D) if mask >> e & 1]))
+            field = rng.uniform(-2.5 * dims[dim], 2.5 * dims[dim], nf)
+            field[:: 7] = np.round(field[:: 7])  # some integer (copy) lines
+            variants.append(("field", 0.0, field, mask))
+            if 0 in others:
+                mask0 = 1  # per-lane field over dim 0 only
+                f0 = rng.uniform(-1.6, 1.6, dims[0])
+                variants.append(("lane", 0.0, f0, mask0))
+        for name, shift, field, mask in variants:
+            g.set_coeffs(c)
+            g.advect(dim, shift=shift, field=field, field_mask=mask)
+            got = g.get_coeffs()
+            ref = oracle.advect(ref_in, dims, k, dim, shift=shift, field=field, field_mask=mask,
+                                n_double=n_double(precision, K))
+            assert_parity(got, ref, K, precision, f"dims={dims} k={k} dim={dim} {name}")
+    g.destroy()
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+def test_integer_shifts_bit_exact(precision):
+    """Integer nu is an exact permutation, incl. -0.0 and tiny-negative nu."""
+    dims, k = [40, 12, 6], 3
+    K = k ** 3
+    c = sldg_inputs.random_coeffs(dims, k, 7008)
+    c[5, 3] = -0.0
+    c[7, 0] = -0.0
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision)
+    for dim, nu in [(0, 3.0), (0, -41.0), (1, 5.0), (2, -1.0), (2, 0.0), (1, -1e-20)]:
+        g.set_coeffs(c)
+        g.advect(dim, shift=nu)
+        got = g.get_coeffs()
+        ref = oracle.advect(ref_in, dims, k, dim, shift=nu, n_double=n_double(precision, K))
+        assert got.tobytes() == ref.tobytes(), (dim, nu)
+    g.destroy()
+
+
+def test_c1_config_100_steps():
+    """BASELINE configs[0]: 1D, 64 cells, k=4, nu=0.37, 100 steps, IC 1 + sin(2 pi x)/2."""
+    N, k, nu = 64, 4, 0.37
+    c0 = sldg_inputs.project_1d(lambda x: 1.0 + 0.5 * np.sin(2 * np.pi * x), N, 0.0, 1.0, k, 12)
+    for precision in ["mixed", "fp64"]:
+        nd = n_double(precision, k)
+        g = _Grid([N], k, precision=precision)
+        g.set_coeffs(c0)
+        ref = oracle.round_layout(c0, k, nd)
+        g.advect(0, shift=nu)
+        ref1 = oracle.advect(ref, [N], k, 0, shift=nu, n_double=nd)
+        assert_parity(g.get_coeffs(), ref1, k, precision, "C1 step 1")
+        ref = ref1
+        for _ in range(99):
+            g.advect(0, shift=nu)
+            ref = oracle.advect(ref, [N], k, 0, shift=nu, n_double=nd)
+        got = g.get_coeffs()
+        # multi-step: L2 distance and mass drift, not per-ulp
+        assert oracle.l2_norm_diff(got, ref, 1.0 / N, k) < (1e-12 if precision == "fp64" else 1e-7)
+        m0 = oracle.mass(oracle.round_layout(c0, k, nd), k, 1.0 / N)
+        assert abs(g.mass() - m0) / m0 < 1e-14
+        exact = sldg_inputs.project_1d(lambda x: 1.0 + 0.5 * np.sin(2 * np.pi * (x - nu * 100 / N)),
+                                       N, 0.0, 1.0, k, 12)
+        err = oracle.l2_norm_diff(got, exact, 1.0 / N, k)
+        assert err < 1e-8, err  # SURVEY P17 magnitude ~3e-9
+        g.destroy()
+
+
+def test_mass_and_drift_1000_steps():
+    """Mass conserved to fp64 accuracy: mixed 2D Landau, 500 split steps
+    (1000 sweeps) with per-line fields: relative drift <= 1e-12 (north_star)."""
+    dims, k = [64, 64], 4
+    kinds, lo, hi = ["x", "v"], [0.0, -6.0], [4 * np.pi, 6.0]
+    terms = sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=0.5)
+    c = sldg_inputs.assemble_separable(terms, dims, k)
+    g = _Grid(dims, k, lo=lo, hi=hi, precision="mixed")
+    g.set_coeffs(c)
+    vol = (hi[0] - lo[0]) / 64 * (hi[1] - lo[1]) / 64
+    ref = oracle.round_layout(c, k * k, 1)
+    m0 = oracle.mass(ref, k * k, vol)
+    assert abs(g.mass() - m0) <= 1e-13 * abs(m0)
+    sweeps = sldg_inputs.vlasov_fields(dims, kinds, lo, hi, eps=0.5)
+    for _ in range(500):
+        for d, f, mask in sweeps:
+            g.advect(d, field=f, field_mask=mask)
+    assert abs(g.mass() - m0) / abs(m0) <= 1e-12
+
+
+def test_mass_matches_oracle():
+    for dims, k, prec in [([1000], 3, "mixed"), ([50, 30, 7], 2, "fp64"), ([17, 9, 5, 4], 2, "mixed")]:
+        K = k ** len(dims)
+        c = sldg_inputs.random_coeffs(dims, k, 3)
+        g = _Grid(dims, k, lo=[-1.0] * len(dims), hi=[2.0] * len(dims), precision=prec)
+        g.set_coeffs(c)
+        vol = np.prod([3.0 / n for n in dims])
+        ref = oracle.mass(oracle.round_layout(c, K, n_double(prec, K)), K, vol)
+        assert abs(g.mass() - ref) <= 1e-13 * abs(ref)
+        g.destroy()
+
+
+# ------------------------------------------------------------------------------ set / get / fill
+def test_set_get_roundtrip_and_validation():
+    from paper_1603_07008_b200 import SldgError
+    dims, k = [20, 6], 2
+    K = 4
+    c = sldg_inputs.random_coeffs(dims, k, 1)
+    c[3, 1] = 0.1
+    c[4, 2] = 2.0 ** -150  # rounds to 0 or the smallest subnormal (RNE)
+    g = _Grid(dims, k, precision="mixed")
+    g.set_coeffs(c)
+    got = g.get_coeffs()
+    assert got[:, 0].tobytes() == c[:, 0].tobytes()  # fp64 slot bit-exact
+    assert got[:, 1:].tobytes() == c[:, 1:].astype(np.float32).astype(np.float64).tobytes()
+    # partial ranges
+    part = g.get_coeffs(37, 50)
+    assert part.tobytes() == got[37:87].tobytes()
+    g.set_coeffs(np.zeros((5, K)), first_cell=100)
+    assert np.all(g.get_coeffs(100, 5) == 0)
+    before = g.get_coeffs()
+    bad = c.copy()
+    bad[10, 0] = np.nan
+    with pytest.raises(SldgError):
+        g.set_coeffs(bad)
+    bad = c.copy()
+    bad[11, 3] = 1e39
+    with pytest.raises(SldgError):
+        g.set_coeffs(bad)
+    with pytest.raises(SldgError):
+        g.set_coeffs(c[:10], first_cell=115)
+    with pytest.raises(SldgError):
+        g.advect(0, shift=float("inf"))
+    with pytest.raises(SldgError):
+        g.advect(0, field=np.zeros(20), field_mask=0b01)
+    with pytest.raises(SldgError):
+        g.advect(1, field=np.array([0.5, np.nan] * 10), field_mask=0b01)
+    with pytest.raises(SldgError):
+        g.advect(2, shift=0.5)
+    assert g.get_coeffs().tobytes() == before.tobytes()  # EINVAL changed nothing
+    g.destroy()
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+def test_fill_random_bit_exact(precision):
+    dims, k = [37, 11, 6], 3
+    K = 27
+    g = _Grid(dims, k, precision=precision)
+    g.fill_random(1603)
+    ref = oracle_input(sldg_inputs.random_coeffs(dims, k, 1603), K, precision)
+    assert g.get_coeffs().tobytes() == ref.tobytes()
+    g.destroy()
+
+
+def test_fill_separable():
+    dims, k = [16, 12], 4
+    kinds, lo, hi = ["x", "v"], [0.0, -6.0], [4 * np.pi, 6.0]
+    terms = sldg_inputs.landau_terms(dims, k, kinds, lo, hi)
+    g = _Grid(dims, k, lo=lo, hi=hi, precision="fp64")
+    g.fill_separable(terms)
+    ref = sldg_inputs.assemble_separable(terms, dims, k)
+    np.testing.assert_allclose(g.get_coeffs(), ref, rtol=0, atol=1e-15)
+    g.destroy()
+
+
+def test_device_field_and_sticky_error():
+    from paper_1603_07008_b200 import SldgError
+    dims, k = [64, 32], 3
+    K = 9
+    c = sldg_inputs.random_coeffs(dims, k, 5)
+    g = _Grid(dims, k, precision="mixed")
+    g.set_coeffs(c)
+    field = np.linspace(-5.5, 7.25, 32)
+    tf = torch.tensor(field, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    g.advect_device(0, tf.data_ptr(), 0b10)
+    ref = oracle.advect(oracle_input(c, K, "mixed"), dims, k, 0, field=field, field_mask=0b10, n_double=1)
+    assert_parity(g.get_coeffs(), ref, K, "mixed", "device field")
+    bad = tf.clone()
+    bad[3] = float("nan")
+    torch.cuda.synchronize()
+    before = g.get_coeffs()
+    g.advect_device(0, bad.data_ptr(), 0b10)
+    with pytest.raises(SldgError):
+        g.sync()
+    after = g.get_coeffs()  # flag was reset by the failing sync
+    v = after.reshape(32, 64, K)
+    b = before.reshape(32, 64, K)
+    assert v[3].tobytes() == b[3].tobytes()  # the invalid line was left unchanged
+    g.destroy()
+
+
+# ------------------------------------------------------------------------------ properties
+def test_convergence_order_fp64():
+    """P11 on the GPU path: order k on smooth data, fixed CFL 0.8, one period."""
+    for k in [2, 3, 4]:
+        errs = []
+        for N in [40, 80, 160]:
+            c0 = sldg_inputs.project_1d(lambda x: np.sin(2 * np.pi * x), N, 0.0, 1.0, k, 12)
+            g = _Grid([N], k, precision="fp64")
+            g.set_coeffs(c0)
+            for _ in range(N * 5 // 4):
+                g.advect(0, shift=0.8)
+            errs.append(oracle.l2_norm_diff(g.get_coeffs(), c0, 1.0 / N, k))
+            g.destroy()
+        orders = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+        assert orders.min() >= k - 0.3, (k, errs)
+
+
+# ------------------------------------------------------------------------------ full sizes
+def _line_cells(dims, dim, perp):
+    """Global cell indices of the line along `dim` with perpendicular indices perp (dict)."""
+    S = np.cumprod([1] + list(dims[:-1]))
+    base = sum(perp[e] * S[e] for e in perp)
+    return base + np.arange(dims[dim]) * S[dim]
+
+
+def _sampled_line_parity(g, dims, k, precision, dim, field, mask, seed, n_lines, rng):
+    D, K = len(dims), k ** len(dims)
+    nd = n_double(precision, K)
+    fd = [e for e in range(D) if mask >> e & 1]
+    for _ in range(n_lines):
+        perp = {e: int(rng.integers(0, dims[e])) for e in range(D) if e != dim}
+        cells = _line_cells(dims, dim, perp)
+        src = oracle.round_layout(sldg_inputs.random_coeffs(dims, k, seed, cells=cells), K, nd)
+        fi, st = 0, 1
+        for e in fd:
+            fi += perp[e] * st
+            st *= dims[e]
+        nu = float(field[fi]) if field is not None else 0.0
+        ldims = [1] * D
+        ldims[dim] = dims[dim]
+        ref = oracle.advect(src, ldims, k, dim, shift=nu, n_double=nd)
+        got = np.concatenate([g.get_coeffs(int(c), 1) for c in cells]) if dim > 0 else \
+            g.get_coeffs(int(cells[0]), dims[0])
+        assert_parity(got, ref, K, precision, f"line dim={dim} perp={perp}")
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+def test_c2_full_grid(precision):
+    """BASELINE configs[1]: 2D 1024^2, k=4, v-dependent x-shift + E(x)-dependent v-shift,
+    full-grid element-wise parity."""
+    dims, k = [1024, 1024], 4
+    K = 16
+    kinds, lo, hi = ["x", "v"], [0.0, -6.0], [4 * np.pi, 6.0]
+    c = sldg_inputs.random_coeffs(dims, k, 1603)
+    g = _Grid(dims, k, lo=lo, hi=hi, precision=precision)
+    g.set_coeffs(c)
+    ref = oracle_input(c, K, precision)
+    for d, f, mask in sldg_inputs.vlasov_fields(dims, kinds, lo, hi, eps=0.5):
+        g.advect(d, field=f, field_mask=mask)
+        ref = oracle.advect(ref, dims, k, d, field=f, field_mask=mask, n_double=n_double(precision, K))
+        assert_parity(g.get_coeffs(), ref, K, precision, f"C2 sweep {d}")
+        g.set_coeffs(oracle_input(ref, K, precision))  # re-sync state: one-sweep parity each time
+    g.destroy()
+
+
+@pytest.mark.parametrize("k", [2, 6])
+def test_c3_order_sweep_sampled(k):
+    """BASELINE configs[2]: 2D 4096^2, nu = 2.37 along dim 0 and dim 1, mixed; sampled lines."""
+    dims = [4096, 4096]
+    g = _Grid(dims, k, precision="mixed")
+    rng = np.random.default_rng(k)
+    for dim in [0, 1]:
+        g.fill_random(7008)
+        g.advect(dim, shift=2.37)
+        _sampled_line_parity(g, dims, k, "mixed", dim, np.array([2.37]), 0, 7008, 6, rng)
+    g.destroy()
+
+
+def test_c5_full_size_sampled_lines():
+    """BASELINE configs[4]: 4D 128^4, k=3, mixed, in the bench's launch configuration (one
+    GPU, ping-pong): every sweep of the split step on the random parity input, sampled lines
+    recomputed by the oracle (the update is line-local)."""
+    dims, k = [128, 128, 128, 128], 3
+    kinds = ["x", "x", "v", "v"]
+    lo, hi = [0, 0, -6, -6], [4 * np.pi, 4 * np.pi, 6, 6]
+    g = _Grid(dims, k, lo=lo, hi=hi, precision="mixed")
+    rng = np.random.default_rng(5)
+    for d, f, mask in sldg_inputs.vlasov_fields(dims, kinds, lo, hi, eps=0.5):
+        g.fill_random(1603)
+        g.advect(d, field=f, field_mask=mask)
+        _sampled_line_parity(g, dims, k, "mixed", d, f, mask, 1603, 3, rng)
+    g.destroy()
