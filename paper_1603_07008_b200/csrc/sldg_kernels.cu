@@ -1,12 +1,9 @@
-// sldg_kernels.cu -- sm_100a kernels of the mixed-precision SLDG step (arXiv:1603.07008).
-//
-// Hot path:
+// sldg_kernels.cu -- sm_100a kernels of the mixed-precision SLDG step (arXiv:1603.07008),
+// everything except the sweeps themselves (those are in sldg_sweep.cu):
 //   build_weights   a1 shift decomposition + a2 weight build (A, B per field entry)
-//   sweep_d0        a3-a7 for the contiguous dim 0 (lane = target cell, neighbour source by
-//                   warp shuffle, every slot read from HBM once)
-//   sweep_strided   a3-a7 for dims >= 1 (lane = consecutive i_0 so every warp access is a
-//                   coalesced row segment; register sliding window of T targets along dim)
-// Auxiliary: mass reduction (a9), set/get conversion, synthetic fills.
+//   mass            a9 deterministic fp64 reduction of the mass slot
+//   set / get       host AoS fp64 <-> device split layout (RNE narrowing)
+//   fills           synthetic inputs (counter-based random, separable Landau)
 //
 // Arithmetic is fp64 throughout (reading R6): fp32 slots are promoted exactly on load and
 // rounded to nearest-even on store (__double2float_rn; no fast-math, no FTZ).
@@ -17,31 +14,6 @@
 #include "sldg_internal.h"
 
 namespace sldg {
-
-// ============================================================================================
-// Element access
-// ============================================================================================
-template <int PREC>
-__device__ __forceinline__ double ld_slot(const Arrays& a, const Layout& L, int q, int64_t layerp,
-                                          int64_t inner)
-{
-    if (PREC == SLDG_FP64) return __ldg(&a.s64[(layerp * L.K + q) * L.L + inner]);
-    if (q == 0) return __ldg(&a.mass[layerp * L.L + inner]);
-    return (double)__ldg(&a.pl[(layerp * (L.K - 1) + (q - 1)) * L.L + inner]);
-}
-
-template <int PREC>
-__device__ __forceinline__ void st_slot(const Arrays& a, const Layout& L, int q, int64_t layerp,
-                                        int64_t inner, double v)
-{
-    if (PREC == SLDG_FP64) {
-        __stcs(&a.s64[(layerp * L.K + q) * L.L + inner], v);
-    } else if (q == 0) {
-        __stcs(&a.mass[layerp * L.L + inner], v);
-    } else {
-        __stcs(&a.pl[(layerp * (L.K - 1) + (q - 1)) * L.L + inner], __double2float_rn(v));
-    }
-}
 
 // ============================================================================================
 // a1 + a2: shift decomposition and weight build, one thread per field entry.
@@ -189,294 +161,6 @@ cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field,
 }
 
 // ============================================================================================
-// Field index of a line from its perpendicular indices.
-// ============================================================================================
-__device__ __forceinline__ int64_t field_index(const Sweep& sw, const int64_t* idx, int D)
-{
-    int64_t f = 0;
-    if (sw.fmask) {
-#pragma unroll
-        for (int e = 0; e < kMaxDim; ++e)
-            if (e < D) f += idx[e] * sw.fstride[e];
-    }
-    return f;
-}
-
-// ============================================================================================
-// a3-a7 along the contiguous dim 0.  One thread = one target cell (all k^{D-1} coupled
-// groups); lanes hold consecutive cells of a line so the B-source row of the warp is one
-// contiguous segment, and each lane's A-source (i - i* - 1) is its left neighbour's B-source
-// (i - 1 - i*), received by __shfl_up (neighbour reuse).  Lanes whose neighbour
-// is not in the warp/line load it themselves.
-// ============================================================================================
-template <int KK, int PREC>
-__global__ void __launch_bounds__(256) sweep_d0_kernel(Layout lay, Sweep sw, Arrays src, Arrays dst,
-                                                       int64_t layer_begin, int64_t layer_end)
-{
-    const int64_t L = lay.L;
-    const int64_t n0 = lay.n[0];
-    const int64_t total = (layer_end - layer_begin) * L;
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (total == 0) return;
-    const bool active = t < total;
-    if (!active) t = total - 1;  // inactive lanes still take part in the shuffles
-    const int64_t layer = layer_begin + t / L;
-    const int64_t inner = t - (t / L) * L;
-    const int64_t i0 = inner % n0;
-
-    int64_t idx[kMaxDim];
-    {
-        int64_t rem = inner;
-#pragma unroll
-        for (int e = 0; e < kMaxDim; ++e) {
-            if (e < lay.D - 1 || (lay.D == 1 && e == 0)) {
-                idx[e] = rem % lay.n[e];
-                rem /= lay.n[e];
-            } else {
-                idx[e] = 0;
-            }
-        }
-        if (lay.D >= 2) idx[lay.D - 1] = lay.first_layer + layer;
-    }
-    const int64_t f = field_index(sw, idx, lay.D);
-    const int64_t s = __ldg(&sw.smod[f]);
-    const int cp = __ldg(&sw.copy[f]);
-    const double* __restrict__ w = sw.ab + f * (2 * KK * KK);
-
-    int64_t iB = i0 - s;
-    if (iB < 0) iB += n0;
-    int64_t iA = iB - 1;
-    if (iA < 0) iA += n0;
-    const int64_t base = inner - i0;
-    const int lane = threadIdx.x & 31;
-    const bool from_nbr = (lane > 0) && (i0 > 0);
-    const int64_t layerp = lay.pad + layer;
-    const int G = lay.K / KK;
-
-#pragma unroll 1
-    for (int g = 0; g < G; ++g) {
-        double a[KK], b[KK];
-#pragma unroll
-        for (int j = 0; j < KK; ++j) b[j] = ld_slot<PREC>(src, lay, g * KK + j, layerp, base + iB);
-#pragma unroll
-        for (int j = 0; j < KK; ++j) {
-            double v = __shfl_up_sync(0xffffffffu, b[j], 1);
-            if (!from_nbr) v = ld_slot<PREC>(src, lay, g * KK + j, layerp, base + iA);
-            a[j] = v;
-        }
-        if (active) {
-#pragma unroll
-            for (int j = 0; j < KK; ++j) {
-                double o;
-                if (cp) {
-                    o = b[j];
-                } else {
-                    o = 0.0;
-#pragma unroll
-                    for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[j * KK + l]), a[l], o);
-#pragma unroll
-                    for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[KK * KK + j * KK + l]), b[l], o);
-                }
-                st_slot<PREC>(dst, lay, g * KK + j, layerp, inner, o);
-            }
-        }
-    }
-}
-
-// ============================================================================================
-// a3-a7 along a strided dim d >= 1.  One thread = (i_0, other perpendicular indices,
-// segment of T consecutive targets along d, one coupled group).  Lanes run along i_0, so
-// every load/store instruction of a warp touches one contiguous row segment (coalesced) even
-// when the line shifts differ per lane (per-lane CFL fields).  Along the segment each source
-// row is loaded once and reused as the next target's A-source (register sliding window).
-// ============================================================================================
-template <int KK, int PREC, int T>
-__global__ void __launch_bounds__(256) sweep_strided_kernel(Layout lay, Sweep sw, Arrays src, Arrays dst,
-                                                            int64_t layer_begin, int64_t layer_end)
-{
-    const int D = lay.D;
-    const int d = sw.dim;
-    const bool outer = (d == D - 1);
-    const int64_t nlay = layer_end - layer_begin;
-    const int64_t nline = outer ? nlay : sw.nd;  // targets along the line handled here
-    const int64_t nseg = (nline + T - 1) / T;
-    int G = 1;
-    for (int e = 0; e < D - 1; ++e) G *= KK;
-
-    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    int64_t idx[kMaxDim];
-    int64_t rem = t;
-    idx[0] = rem % lay.n[0];
-    rem /= lay.n[0];
-#pragma unroll
-    for (int e = 1; e < kMaxDim; ++e) {
-        idx[e] = 0;
-        if (e < D - 1 && e != d) {
-            idx[e] = rem % lay.n[e];
-            rem /= lay.n[e];
-        }
-    }
-    int64_t layer = 0;
-    if (!outer) {
-        layer = layer_begin + rem % nlay;
-        rem /= nlay;
-        idx[D - 1] = lay.first_layer + layer;
-    }
-    const int64_t seg = rem % nseg;
-    rem /= nseg;
-    const int64_t g = rem;
-    if (g >= G || nlay == 0) return;
-
-    // coupled group g -> base slot (digits of g over dims e != d, ascending)
-    int qbase = 0, kd = 1;
-    {
-        int gg = (int)g, kp = 1;
-        for (int e = 0; e < D; ++e) {
-            if (e == d) {
-                kd = kp;
-            } else {
-                qbase += (gg % KK) * kp;
-                gg /= KK;
-            }
-            kp *= KK;
-        }
-    }
-
-    idx[d] = 0;
-    const int64_t f = field_index(sw, idx, D);
-    const int cp = __ldg(&sw.copy[f]);
-    const double* __restrict__ w = sw.ab + f * (2 * KK * KK);
-
-    // inner offset of the line start (i_d = 0) and stride along the line
-    int64_t inner0 = 0;
-    for (int e = 0; e < D - 1; ++e) inner0 += idx[e] * lay.S[e];
-    const int64_t step = outer ? 0 : lay.S[d];
-
-    // first target (line coordinate) and source positions
-    const int64_t t0 = seg * T;  // local target index along the line
-    int64_t nt = nline - t0;
-    if (nt > T) nt = T;
-
-    // source line coordinate of the A-source of target t0:  (tg - i* - 1)
-    int64_t sp;  // source position in "line coordinates" (layer index for outer, i_d otherwise)
-    if (outer) {
-        const int64_t tg = lay.first_layer + layer_begin + t0;  // global target layer
-        if (sw.wrap) {
-            int64_t s = __ldg(&sw.smod[f]);
-            sp = tg - s - 1;
-            sp %= sw.nd;
-            if (sp < 0) sp += sw.nd;
-        } else {
-            sp = tg - __ldg(&sw.shift[f]) - 1 - lay.first_layer;  // local layer (may be halo)
-        }
-    } else {
-        int64_t s = __ldg(&sw.smod[f]);
-        sp = t0 - s - 1;
-        if (sp < 0) sp += sw.nd;
-    }
-
-    double v[T + 1][KK];
-#pragma unroll
-    for (int p = 0; p <= T; ++p) {
-        if (p <= nt) {
-            int64_t lp, in;
-            if (outer) {
-                lp = lay.pad + sp;
-                in = inner0;
-            } else {
-                lp = lay.pad + layer;
-                in = inner0 + sp * step;
-            }
-#pragma unroll
-            for (int j = 0; j < KK; ++j) v[p][j] = ld_slot<PREC>(src, lay, qbase + j * kd, lp, in);
-        }
-        ++sp;
-        if (sw.wrap && sp == sw.nd) sp = 0;
-    }
-#pragma unroll
-    for (int p = 1; p <= T; ++p) {
-        if (p <= nt) {
-            const int64_t tl = t0 + p - 1;
-            int64_t lp, in;
-            if (outer) {
-                lp = lay.pad + layer_begin + tl;
-                in = inner0;
-            } else {
-                lp = lay.pad + layer;
-                in = inner0 + tl * step;
-            }
-#pragma unroll
-            for (int j = 0; j < KK; ++j) {
-                double o;
-                if (cp) {
-                    o = v[p][j];
-                } else {
-                    o = 0.0;
-#pragma unroll
-                    for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[j * KK + l]), v[p - 1][l], o);
-#pragma unroll
-                    for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[KK * KK + j * KK + l]), v[p][l], o);
-                }
-                st_slot<PREC>(dst, lay, qbase + j * kd, lp, in, o);
-            }
-        }
-    }
-}
-
-template <int KK, int PREC>
-static cudaError_t launch_sweep_k(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
-                                  int64_t lb, int64_t le, cudaStream_t s)
-{
-    const int threads = 256;
-    if (sw.dim == 0) {
-        int64_t total = (le - lb) * lay.L;
-        if (total == 0) return cudaSuccess;
-        int64_t blocks = (total + threads - 1) / threads;
-        sweep_d0_kernel<KK, PREC><<<(unsigned)blocks, threads, 0, s>>>(lay, sw, src, dst, lb, le);
-    } else {
-        constexpr int T = (KK <= 2) ? 16 : (KK <= 4 ? 8 : 4);
-        const bool outer = (sw.dim == lay.D - 1);
-        int64_t nline = outer ? (le - lb) : sw.nd;
-        int64_t nseg = (nline + T - 1) / T;
-        int64_t perp = 1;  // perpendicular lines (excluding the layer dim)
-        for (int e = 0; e < lay.D - 1; ++e)
-            if (e != sw.dim) perp *= lay.n[e];
-        int64_t G = 1;
-        for (int e = 0; e < lay.D - 1; ++e) G *= KK;
-        int64_t total = perp * (outer ? 1 : (le - lb)) * nseg * G;
-        if (total == 0) return cudaSuccess;
-        int64_t blocks = (total + threads - 1) / threads;
-        sweep_strided_kernel<KK, PREC, T><<<(unsigned)blocks, threads, 0, s>>>(lay, sw, src, dst, lb, le);
-    }
-    return cudaGetLastError();
-}
-
-template <int PREC>
-static cudaError_t launch_sweep_p(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
-                                  int64_t lb, int64_t le, cudaStream_t s)
-{
-    switch (lay.k) {
-        case 1: return launch_sweep_k<1, PREC>(lay, sw, src, dst, lb, le, s);
-        case 2: return launch_sweep_k<2, PREC>(lay, sw, src, dst, lb, le, s);
-        case 3: return launch_sweep_k<3, PREC>(lay, sw, src, dst, lb, le, s);
-        case 4: return launch_sweep_k<4, PREC>(lay, sw, src, dst, lb, le, s);
-        case 5: return launch_sweep_k<5, PREC>(lay, sw, src, dst, lb, le, s);
-        case 6: return launch_sweep_k<6, PREC>(lay, sw, src, dst, lb, le, s);
-        case 7: return launch_sweep_k<7, PREC>(lay, sw, src, dst, lb, le, s);
-        case 8: return launch_sweep_k<8, PREC>(lay, sw, src, dst, lb, le, s);
-    }
-    return cudaErrorInvalidValue;
-}
-
-cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
-                         int64_t layer_begin, int64_t layer_end, cudaStream_t s, int* n_launched)
-{
-    *n_launched = (layer_end > layer_begin) ? 1 : 0;
-    if (lay.prec == SLDG_FP64) return launch_sweep_p<SLDG_FP64>(lay, sw, src, dst, layer_begin, layer_end, s);
-    return launch_sweep_p<SLDG_MIXED>(lay, sw, src, dst, layer_begin, layer_end, s);
-}
-
-// ============================================================================================
 // a9: mass = sum of slot 0 over local cells, fixed-order two-pass reduction with Neumaier
 // compensation per thread (deterministic for a fixed grid: kMassBlocks x 256 threads).
 // ============================================================================================
@@ -611,9 +295,21 @@ __global__ void fill_random_kernel(Layout lay, Arrays a, uint64_t seed)
             deg += qq % lay.k;
             qq /= lay.k;
         }
+        // n0^deg as the correctly rounded double of the exact integer while it fits in 64 bits
+        // (matches Python's float(n0**deg)); beyond that, exact double products (exact for
+        // power-of-two n0, the only case where the integer exceeds 2^64 in the configs).
         uint64_t p = 1;
-        for (int i = 0; i < deg; ++i) p *= (uint64_t)lay.n[0];
-        v = __ddiv_rn(r, __ull2double_rn(p));
+        double pd = 1.0;
+        bool wide = false;
+        for (int i = 0; i < deg; ++i) {
+            if (!wide && p > UINT64_MAX / (uint64_t)lay.n[0]) {
+                wide = true;
+                pd = __ull2double_rn(p);
+            }
+            if (wide) pd = __dmul_rn(pd, (double)lay.n[0]);
+            else p *= (uint64_t)lay.n[0];
+        }
+        v = __ddiv_rn(r, wide ? pd : __ull2double_rn(p));
     }
     int64_t layer = cell / lay.L, inner = cell - layer * lay.L;
     int64_t lp = lay.pad + layer;

@@ -1,0 +1,429 @@
+// sldg_sweep.cu -- the SLDG sweep kernels for sm_100a.
+//
+// One sweep along dim d applies, for every line (fixed perpendicular indices) and every
+// coupled group (the k slots that differ only in m_d), the update (SS II-A)
+//     c'_{i,j} = sum_l A_jl c_{(i-i*-1) mod n, l} + sum_l B_jl c_{(i-i*) mod n, l}
+// in fp64 (reading R6), with the exact copy c'_i = c_{(i-i*) mod n} when alpha = 0 (R4).
+// Every stored coefficient is read from HBM once and written once.
+//
+//   sweep_d0_kernel       d = 0 (contiguous).  Lane = target cell, so the warp's B-source row
+//                         is one contiguous segment; the A-source of lane i is the B-source of
+//                         lane i-1 (__shfl_up, the neighbour reuse of P:310-317).  Each thread
+//                         does all k^{D-1} coupled groups of its cell, GB groups per batch with
+//                         all loads issued before any use (memory-level parallelism).
+//   sweep_strided_kernel  d >= 1.  Lane = consecutive i_0 (every warp access is a coalesced row
+//                         segment even for per-lane CFL fields); each thread walks T consecutive
+//                         targets along d for ALL coupled groups of its line, keeping the line's
+//                         A/B in registers (loaded once, amortised over k^{D-1} groups x T
+//                         targets) and reusing each source row as the next target's A-source.
+// Values stay in their storage type in registers (fp32 slots as float) and are promoted at
+// the FMA (exact), which halves the registers that hold loads in flight.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "sldg_internal.h"
+
+namespace sldg {
+
+// ---- element access --------------------------------------------------------------------
+// mixed: slot 0 at mass[layerp*L + inner]; slot q >= 1 at pl[(layerp*(K-1) + q-1)*L + inner]
+// fp64 : slot q at s64[(layerp*K + q)*L + inner]
+template <int PREC>
+__device__ __forceinline__ int64_t off_m(const Layout& L, int64_t layerp, int64_t inner)
+{
+    return (PREC == SLDG_FP64) ? layerp * (int64_t)L.K * L.L + inner : layerp * L.L + inner;
+}
+template <int PREC>
+__device__ __forceinline__ int64_t off_f(const Layout& L, int64_t layerp, int64_t inner)
+{
+    return (PREC == SLDG_FP64) ? 0 : layerp * (int64_t)(L.K - 1) * L.L + inner;
+}
+
+__device__ __forceinline__ int64_t field_index(const Sweep& sw, const int64_t* idx, int D)
+{
+    int64_t f = 0;
+#pragma unroll
+    for (int e = 0; e < kMaxDim; ++e)
+        if (e < D) f += idx[e] * sw.fstride[e];
+    return f;
+}
+
+// Value held for slot j of a coupled group: fp64 for the fp64 variant and for the mass slot
+// (j == 0 of the mass group), fp32 otherwise.
+template <int PREC, bool MASSG, int J>
+struct VT {
+    using type = typename std::conditional<(PREC == SLDG_FP64) || (MASSG && J == 0), double, float>::type;
+};
+
+// ============================================================================================
+// d = 0
+// ============================================================================================
+// One batch of GB coupled groups g0..g0+GB-1 (slots (g0+gb)*KK + j) of one target cell.
+template <int KK, int PREC, int GB, bool MASSG>
+__device__ __forceinline__ void d0_batch(const Arrays& src, const Arrays& dst, int64_t L, int g0, int G,
+                                         int64_t mB, int64_t fB, int64_t mA, int64_t fA, int64_t mT, int64_t fT,
+                                         bool from_nbr, bool active, int cp, const double* __restrict__ w)
+{
+    // loads: B-source of this lane for every slot of the batch
+    double b[GB][KK];
+#pragma unroll
+    for (int gb = 0; gb < GB; ++gb)
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            const int q = (g0 + gb) * KK + j;
+            double v = 0.0;
+            if (g0 + gb < G) {
+                if (PREC == SLDG_FP64) v = __ldg(src.s64 + mB + (int64_t)q * L);
+                else if (MASSG && gb == 0 && j == 0) v = __ldg(src.mass + mB);
+                else v = (double)__ldg(src.pl + fB + (int64_t)(q - 1) * L);
+            }
+            b[gb][j] = v;
+        }
+    // A-source = left neighbour's B-source
+    double a[GB][KK];
+#pragma unroll
+    for (int gb = 0; gb < GB; ++gb)
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            const int q = (g0 + gb) * KK + j;
+            double v = __shfl_up_sync(0xffffffffu, b[gb][j], 1);
+            if (!from_nbr && g0 + gb < G) {
+                if (PREC == SLDG_FP64) v = __ldg(src.s64 + mA + (int64_t)q * L);
+                else if (MASSG && gb == 0 && j == 0) v = __ldg(src.mass + mA);
+                else v = (double)__ldg(src.pl + fA + (int64_t)(q - 1) * L);
+            }
+            a[gb][j] = v;
+        }
+    if (!active) return;
+#pragma unroll
+    for (int gb = 0; gb < GB; ++gb) {
+        if (g0 + gb >= G) break;
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            const int q = (g0 + gb) * KK + j;
+            double o;
+            if (cp) {
+                o = b[gb][j];
+            } else {
+                o = 0.0;
+#pragma unroll
+                for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[j * KK + l]), a[gb][l], o);
+#pragma unroll
+                for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[KK * KK + j * KK + l]), b[gb][l], o);
+            }
+            if (PREC == SLDG_FP64) __stcs(dst.s64 + mT + (int64_t)q * L, o);
+            else if (MASSG && gb == 0 && j == 0) __stcs(dst.mass + mT, o);
+            else __stcs(dst.pl + fT + (int64_t)(q - 1) * L, __double2float_rn(o));
+        }
+    }
+}
+
+template <int KK, int PREC, int GB>
+__global__ void __launch_bounds__(256) sweep_d0_kernel(Layout lay, Sweep sw, Arrays src, Arrays dst,
+                                                       int64_t layer_begin, int64_t layer_end)
+{
+    const int64_t L = lay.L;
+    const int64_t n0 = lay.n[0];
+    const int64_t total = (layer_end - layer_begin) * L;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const bool active = t < total;
+    if (!active) t = total - 1;  // inactive lanes still take part in the shuffles
+    const int64_t lrel = t / L;
+    const int64_t layer = layer_begin + lrel;
+    const int64_t inner = t - lrel * L;
+    const int64_t i0 = inner % n0;
+
+    int64_t f = 0;
+    if (sw.fmask) {
+        int64_t idx[kMaxDim];
+        int64_t rem = inner;
+#pragma unroll
+        for (int e = 0; e < kMaxDim; ++e) {
+            idx[e] = 0;
+            if (e < lay.D - 1 || (lay.D == 1 && e == 0)) {
+                idx[e] = rem % lay.n[e];
+                rem /= lay.n[e];
+            }
+        }
+        if (lay.D >= 2) idx[lay.D - 1] = lay.first_layer + layer;
+        f = field_index(sw, idx, lay.D);
+    }
+    const int64_t s = __ldg(&sw.smod[f]);
+    const int cp = __ldg(&sw.copy[f]);
+    const double* __restrict__ w = sw.ab + f * (2 * KK * KK);
+
+    int64_t iB = i0 - s;
+    if (iB < 0) iB += n0;
+    int64_t iA = iB - 1;
+    if (iA < 0) iA += n0;
+    const int64_t base = inner - i0;
+    const int lane = threadIdx.x & 31;
+    const bool from_nbr = (lane > 0) && (i0 > 0);
+    const int64_t layerp = lay.pad + layer;
+    const int64_t mB = off_m<PREC>(lay, layerp, base + iB), fB = off_f<PREC>(lay, layerp, base + iB);
+    const int64_t mA = off_m<PREC>(lay, layerp, base + iA), fA = off_f<PREC>(lay, layerp, base + iA);
+    const int64_t mT = off_m<PREC>(lay, layerp, inner), fT = off_f<PREC>(lay, layerp, inner);
+    const int G = lay.K / KK;
+
+    int g0 = 0;
+    if (PREC == SLDG_MIXED) {  // the coupled group holding the fp64 mass slot
+        d0_batch<KK, PREC, 1, true>(src, dst, L, 0, G, mB, fB, mA, fA, mT, fT, from_nbr, active, cp, w);
+        g0 = 1;
+    }
+#pragma unroll 1
+    for (; g0 < G; g0 += GB)
+        d0_batch<KK, PREC, GB, false>(src, dst, L, g0, G, mB, fB, mA, fA, mT, fT, from_nbr, active, cp, w);
+}
+
+// ============================================================================================
+// d >= 1
+// ============================================================================================
+struct LineGeom {
+    int64_t sp0;      // line coordinate of the A-source of the first target
+    int64_t nd;       // line length (for wrapping)
+    int wrap;
+    bool outer;
+    int64_t layerp;   // padded layer of the line (inner sweeps)
+    int64_t inner0;   // inner offset of the line start
+    int64_t step;     // inner stride along the line (inner sweeps)
+    int64_t t_m, t_f; // offsets of the first target
+    int64_t dt_m, dt_f;  // offset step between consecutive targets
+};
+
+template <int PREC>
+__device__ __forceinline__ void src_off(const Layout& lay, const LineGeom& g, int p, int64_t& m, int64_t& f)
+{
+    int64_t c = g.sp0 + p;
+    if (g.wrap) {
+        if (c >= g.nd) c -= g.nd;
+        if (c >= g.nd) c %= g.nd;
+    }
+    if (g.outer) {
+        m = off_m<PREC>(lay, lay.pad + c, g.inner0);
+        f = off_f<PREC>(lay, lay.pad + c, g.inner0);
+    } else {
+        m = off_m<PREC>(lay, g.layerp, g.inner0 + c * g.step);
+        f = off_f<PREC>(lay, g.layerp, g.inner0 + c * g.step);
+    }
+}
+
+template <int KK, int PREC, int T, bool REGW, bool MASSG>
+__device__ __forceinline__ void strided_group(const Layout& lay, const Arrays& src, const Arrays& dst,
+                                              const LineGeom& g, int nt, int qbase, int kd, int cp,
+                                              const double* wr, const double* __restrict__ w)
+{
+    const int64_t L = lay.L;
+    typename VT<PREC, MASSG, 0>::type v0[T + 1];  // slot j = 0 (fp64 if the mass slot)
+    typename VT<PREC, false, 1>::type v[T + 1][KK];  // slots j >= 1 (index 0 unused)
+#pragma unroll
+    for (int p = 0; p <= T; ++p) {
+        int64_t m, f;
+        src_off<PREC>(lay, g, p, m, f);
+        const bool ok = p <= nt;
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            const int q = qbase + j * kd;
+            if (j == 0) {
+                if (PREC == SLDG_FP64) v0[p] = ok ? __ldg(src.s64 + m + (int64_t)q * L) : 0.0;
+                else if (MASSG) v0[p] = ok ? __ldg(src.mass + m) : 0.0;
+                else v0[p] = ok ? __ldg(src.pl + f + (int64_t)(q - 1) * L) : 0.f;
+            } else {
+                if (PREC == SLDG_FP64) v[p][j] = ok ? __ldg(src.s64 + m + (int64_t)q * L) : 0.0;
+                else v[p][j] = ok ? __ldg(src.pl + f + (int64_t)(q - 1) * L) : 0.f;
+            }
+        }
+    }
+#pragma unroll
+    for (int p = 1; p <= T; ++p) {
+        if (p > nt) break;
+        const int64_t tm = g.t_m + (p - 1) * g.dt_m, tf = g.t_f + (p - 1) * g.dt_f;
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            const int q = qbase + j * kd;
+            double o;
+            if (cp) {
+                o = (j == 0) ? (double)v0[p] : (double)v[p][j];
+            } else {
+                o = 0.0;
+#pragma unroll
+                for (int l = 0; l < KK; ++l) {
+                    const double wa = REGW ? wr[j * KK + l] : __ldg(&w[j * KK + l]);
+                    o = fma(wa, (l == 0) ? (double)v0[p - 1] : (double)v[p - 1][l], o);
+                }
+#pragma unroll
+                for (int l = 0; l < KK; ++l) {
+                    const double wb = REGW ? wr[KK * KK + j * KK + l] : __ldg(&w[KK * KK + j * KK + l]);
+                    o = fma(wb, (l == 0) ? (double)v0[p] : (double)v[p][l], o);
+                }
+            }
+            if (PREC == SLDG_FP64) __stcs(dst.s64 + tm + (int64_t)q * L, o);
+            else if (MASSG && j == 0) __stcs(dst.mass + tm, o);
+            else __stcs(dst.pl + tf + (int64_t)(q - 1) * L, __double2float_rn(o));
+        }
+    }
+}
+
+template <int KK, int PREC, int T, bool REGW>
+__global__ void __launch_bounds__(256, 2) sweep_strided_kernel(Layout lay, Sweep sw, Arrays src, Arrays dst,
+                                                               int64_t layer_begin, int64_t layer_end)
+{
+    const int D = lay.D;
+    const int d = sw.dim;
+    const bool outer = (d == D - 1);
+    const int64_t nlay = layer_end - layer_begin;
+    const int64_t nline = outer ? nlay : sw.nd;  // targets along the line handled here
+    const int64_t nseg = (nline + T - 1) / T;
+
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int64_t idx[kMaxDim];
+    int64_t rem = t;
+    idx[0] = rem % lay.n[0];
+    rem /= lay.n[0];
+#pragma unroll
+    for (int e = 1; e < kMaxDim; ++e) {
+        idx[e] = 0;
+        if (e < D - 1 && e != d) {
+            idx[e] = rem % lay.n[e];
+            rem /= lay.n[e];
+        }
+    }
+    int64_t layer = 0;
+    if (!outer) {
+        layer = layer_begin + rem % nlay;
+        rem /= nlay;
+        idx[D - 1] = lay.first_layer + layer;
+    }
+    const int64_t seg = rem;
+    if (seg >= nseg || nlay == 0) return;
+
+    int kd = 1;
+    for (int e = 0; e < d; ++e) kd *= KK;
+    const int G = lay.K / KK;
+
+    idx[d] = 0;
+    const int64_t f = field_index(sw, idx, D);
+    const int cp = __ldg(&sw.copy[f]);
+    const double* __restrict__ w = sw.ab + f * (2 * KK * KK);
+    double wr[REGW ? 2 * KK * KK : 1];
+    if (REGW) {
+#pragma unroll
+        for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&w[i]);
+    }
+
+    LineGeom geo;
+    geo.outer = outer;
+    geo.wrap = sw.wrap;
+    geo.nd = sw.nd;
+    geo.inner0 = 0;
+#pragma unroll
+    for (int e = 0; e < kMaxDim; ++e)
+        if (e < D - 1) geo.inner0 += idx[e] * lay.S[e];
+    geo.step = outer ? 0 : lay.S[d];
+    geo.layerp = lay.pad + layer;
+
+    const int64_t t0 = seg * T;  // first local target along the line
+    const int nt = (int)((nline - t0) < T ? (nline - t0) : T);
+    if (outer) {
+        const int64_t tg = lay.first_layer + layer_begin + t0;
+        if (sw.wrap) {
+            int64_t sp = (tg - __ldg(&sw.smod[f]) - 1) % sw.nd;
+            geo.sp0 = sp < 0 ? sp + sw.nd : sp;
+        } else {
+            geo.sp0 = tg - __ldg(&sw.shift[f]) - 1 - lay.first_layer;  // local (halo) layer
+        }
+        geo.t_m = off_m<PREC>(lay, lay.pad + layer_begin + t0, geo.inner0);
+        geo.t_f = off_f<PREC>(lay, lay.pad + layer_begin + t0, geo.inner0);
+        geo.dt_m = off_m<PREC>(lay, 1, 0) - off_m<PREC>(lay, 0, 0);
+        geo.dt_f = off_f<PREC>(lay, 1, 0) - off_f<PREC>(lay, 0, 0);
+    } else {
+        int64_t sp = t0 - __ldg(&sw.smod[f]) - 1;
+        geo.sp0 = sp < 0 ? sp + sw.nd : sp;
+        geo.t_m = off_m<PREC>(lay, geo.layerp, geo.inner0 + t0 * geo.step);
+        geo.t_f = off_f<PREC>(lay, geo.layerp, geo.inner0 + t0 * geo.step);
+        geo.dt_m = geo.step;
+        geo.dt_f = geo.step;
+    }
+
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+        // coupled group g -> base slot (digits of g over the dims e != d, ascending)
+        int qbase = 0;
+        {
+            int gg = g, kp = 1;
+#pragma unroll
+            for (int e = 0; e < kMaxDim; ++e) {
+                if (e < D && e != d) {
+                    qbase += (gg % KK) * kp;
+                    gg /= KK;
+                }
+                if (e < D) kp *= KK;
+            }
+        }
+        if (PREC == SLDG_MIXED && g == 0)
+            strided_group<KK, PREC, T, REGW, true>(lay, src, dst, geo, nt, qbase, kd, cp, wr, w);
+        else
+            strided_group<KK, PREC, T, REGW, false>(lay, src, dst, geo, nt, qbase, kd, cp, wr, w);
+    }
+}
+
+// ============================================================================================
+// launchers
+// ============================================================================================
+template <int KK, int PREC>
+static cudaError_t launch_sweep_k(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
+                                  int64_t lb, int64_t le, cudaStream_t s)
+{
+    const int threads = 256;
+    if (sw.dim == 0) {
+        constexpr int GB = (KK <= 2) ? 6 : (KK <= 4 ? 12 / KK : 1);
+        int64_t total = (le - lb) * lay.L;
+        if (total == 0) return cudaSuccess;
+        int64_t blocks = (total + threads - 1) / threads;
+        sweep_d0_kernel<KK, PREC, GB><<<(unsigned)blocks, threads, 0, s>>>(lay, sw, src, dst, lb, le);
+    } else {
+        constexpr int T = (KK <= 2) ? 16 : (KK <= 3 ? 8 : 4);
+        const bool outer = (sw.dim == lay.D - 1);
+        int64_t nline = outer ? (le - lb) : sw.nd;
+        int64_t nseg = (nline + T - 1) / T;
+        int64_t perp = 1;  // perpendicular lines inside a layer
+        for (int e = 0; e < lay.D - 1; ++e)
+            if (e != sw.dim) perp *= lay.n[e];
+        int64_t total = perp * (outer ? 1 : (le - lb)) * nseg;
+        if (total == 0) return cudaSuccess;
+        int64_t blocks = (total + threads - 1) / threads;
+        if (KK <= 4)
+            sweep_strided_kernel<KK, PREC, T, true><<<(unsigned)blocks, threads, 0, s>>>(lay, sw, src, dst, lb, le);
+        else
+            sweep_strided_kernel<KK, PREC, T, false><<<(unsigned)blocks, threads, 0, s>>>(lay, sw, src, dst, lb, le);
+    }
+    return cudaGetLastError();
+}
+
+template <int PREC>
+static cudaError_t launch_sweep_p(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
+                                  int64_t lb, int64_t le, cudaStream_t s)
+{
+    switch (lay.k) {
+        case 1: return launch_sweep_k<1, PREC>(lay, sw, src, dst, lb, le, s);
+        case 2: return launch_sweep_k<2, PREC>(lay, sw, src, dst, lb, le, s);
+        case 3: return launch_sweep_k<3, PREC>(lay, sw, src, dst, lb, le, s);
+        case 4: return launch_sweep_k<4, PREC>(lay, sw, src, dst, lb, le, s);
+        case 5: return launch_sweep_k<5, PREC>(lay, sw, src, dst, lb, le, s);
+        case 6: return launch_sweep_k<6, PREC>(lay, sw, src, dst, lb, le, s);
+        case 7: return launch_sweep_k<7, PREC>(lay, sw, src, dst, lb, le, s);
+        case 8: return launch_sweep_k<8, PREC>(lay, sw, src, dst, lb, le, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
+                         int64_t layer_begin, int64_t layer_end, cudaStream_t s, int* n_launched)
+{
+    *n_launched = (layer_end > layer_begin) ? 1 : 0;
+    if (lay.prec == SLDG_FP64) return launch_sweep_p<SLDG_FP64>(lay, sw, src, dst, layer_begin, layer_end, s);
+    return launch_sweep_p<SLDG_MIXED>(lay, sw, src, dst, layer_begin, layer_end, s);
+}
+
+}  // namespace sldg
