@@ -163,6 +163,14 @@ sldg_status sldg_nccl_unique_id(void* out128);
  * (layers below its first layer) and right.  Lines with integer part i* read layers
  * i - i* - 1 and i - i*, so left = max(0, imax + 1), right = max(0, -imin). */
 sldg_status sldg_halo_widths(int64_t imin, int64_t imax, int64_t* left, int64_t* right);
+/* Host-only halo transfer plan of `rank` for a sharded sweep with halo widths (left, right)
+ * and `pad` halo layers per side: 4 int64 per entry {kind, peer, slot, src} where kind 0 =
+ * receive into padded local layer `slot` from `peer`, 1 = send padded local layer `slot` to
+ * `peer`, 2 = copy own padded layer `src` into `slot`.  Entries to/from one peer appear in
+ * the receiver's halo-slot order on both sides (the order NCCL pairs them in).  out == NULL
+ * returns only *n_entries.  This is exactly the plan sldg_advect executes with NCCL. */
+sldg_status sldg_halo_plan(int64_t n, int world, int rank, int64_t pad, int64_t left, int64_t right,
+                           int64_t* out, int64_t max_entries, int64_t* n_entries);
 /* Owner rank and local index of global layer `layer` in a balanced block split of n over
  * world ranks. */
 sldg_status sldg_layer_owner(int64_t n, int world, int64_t layer, int* owner, int64_t* local);

@@ -184,6 +184,48 @@ sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arr
     return SLDG_OK;
 }
 
+// Halo plan for a sweep along the sharded layer dim.  This rank's halo slots are the padded
+// local layers [pad-left, pad) (global layers first-left..first-1) and [pad+layers,
+// pad+layers+right) (global first+layers..), all mod n.  Entries, in an order both sides of
+// every peer pair agree on (the receiver's halo-slot order):
+//   kind 0: receive into padded slot `slot` from rank `peer`
+//   kind 1: send my padded layer `slot` to rank `peer`
+//   kind 2: copy my own padded layer `src` into slot `slot` (wrap-around onto this rank)
+struct Xfer {
+    int kind;
+    int peer;
+    int64_t slot;
+    int64_t src;
+};
+
+std::vector<Xfer> halo_plan(int64_t n, int world, int rank, int64_t pad, int64_t left, int64_t right)
+{
+    std::vector<Xfer> xs;
+    int64_t first, layers;
+    split(n, world, rank, &first, &layers);
+    for (int64_t j = 0; j < left + right; ++j) {
+        int64_t gl = (j < left) ? first - left + j : first + layers + (j - left);
+        int64_t slot = (j < left) ? pad - left + j : pad + layers + (j - left);
+        gl = ((gl % n) + n) % n;
+        int64_t loc = 0;
+        int own = owner_of(n, world, gl, &loc);
+        if (own == rank) xs.push_back({2, rank, slot, pad + loc});
+        else xs.push_back({0, own, slot, 0});
+    }
+    for (int p = 0; p < world; ++p) {
+        if (p == rank) continue;
+        int64_t pf, pc;
+        split(n, world, p, &pf, &pc);
+        for (int64_t j = 0; j < left + right; ++j) {
+            int64_t gl = (j < left) ? pf - left + j : pf + pc + (j - left);
+            gl = ((gl % n) + n) % n;
+            int64_t loc = 0;
+            if (owner_of(n, world, gl, &loc) == rank) xs.push_back({1, p, pad + loc, 0});
+        }
+    }
+    return xs;
+}
+
 // Halo exchange along the sharded layer dim: this rank receives global layers
 // [first-left, first) and [first+layers, first+layers+right) (mod n) into its pad region of
 // `a`, and sends whatever other ranks need from its own layers.  Grouped NCCL send/recv on
@@ -209,55 +251,26 @@ sldg_status halo_exchange(sldg_grid g, const Arrays& a, int64_t left, int64_t ri
             *c1 = pl_elems;
         }
     };
-    struct Xfer {
-        int peer;
-        int64_t lp;  // padded local layer index
-        bool send;
-    };
-    std::vector<Xfer> xs;
-    // receives: my halo slots
-    for (int64_t j = 0; j < left + right; ++j) {
-        int64_t gl, slot;
-        if (j < left) {
-            gl = L.first_layer - left + j;
-            slot = L.pad - left + j;
-        } else {
-            gl = L.first_layer + L.layers + (j - left);
-            slot = L.pad + L.layers + (j - left);
-        }
-        gl = ((gl % n) + n) % n;
-        int64_t loc = 0;
-        int own = owner_of(n, g->world, gl, &loc);
-        if (own == g->rank) {
-            void *d0, *d1, *s0, *s1;
-            size_t c0, c1;
-            layer_ptrs(slot, &d0, &c0, &d1, &c1);
-            layer_ptrs(L.pad + loc, &s0, &c0, &s1, &c1);
-            CU(cudaMemcpyAsync(d0, s0, c0 * (L.prec == SLDG_FP64 ? 8 : 8), cudaMemcpyDeviceToDevice, g->comm_stream));
-            if (d1) CU(cudaMemcpyAsync(d1, s1, c1 * 4, cudaMemcpyDeviceToDevice, g->comm_stream));
-        } else {
-            xs.push_back({own, slot, false});
-        }
+    std::vector<Xfer> xs = halo_plan(n, g->world, g->rank, L.pad, left, right);
+    for (const Xfer& x : xs) {  // layers this rank owns itself (wrap-around): device copies
+        if (x.kind != 2) continue;
+        void *d0, *d1, *s0, *s1;
+        size_t c0, c1;
+        layer_ptrs(x.slot, &d0, &c0, &d1, &c1);
+        layer_ptrs(x.src, &s0, &c0, &s1, &c1);
+        CU(cudaMemcpyAsync(d0, s0, c0 * 8, cudaMemcpyDeviceToDevice, g->comm_stream));
+        if (d1) CU(cudaMemcpyAsync(d1, s1, c1 * 4, cudaMemcpyDeviceToDevice, g->comm_stream));
     }
-    // sends: for every other rank, the layers of mine it needs (same formula, their view)
-    for (int p = 0; p < g->world; ++p) {
-        if (p == g->rank) continue;
-        int64_t pf, pc;
-        split(n, g->world, p, &pf, &pc);
-        for (int64_t j = 0; j < left + right; ++j) {
-            int64_t gl = (j < left) ? pf - left + j : pf + pc + (j - left);
-            gl = ((gl % n) + n) % n;
-            int64_t loc = 0;
-            if (owner_of(n, g->world, gl, &loc) == g->rank) xs.push_back({p, L.pad + loc, true});
-        }
-    }
-    if (xs.empty()) return SLDG_OK;
+    bool any = false;
+    for (const Xfer& x : xs) any |= (x.kind != 2);
+    if (!any) return SLDG_OK;
     NC(ncclGroupStart());
     for (const Xfer& x : xs) {
+        if (x.kind == 2) continue;
         void *p0, *p1;
         size_t c0, c1;
-        layer_ptrs(x.lp, &p0, &c0, &p1, &c1);
-        if (x.send) {
+        layer_ptrs(x.slot, &p0, &c0, &p1, &c1);
+        if (x.kind == 1) {
             NC(ncclSend(p0, c0, ncclFloat64, x.peer, comm, g->comm_stream));
             if (p1) NC(ncclSend(p1, c1, ncclFloat32, x.peer, comm, g->comm_stream));
         } else {
@@ -393,6 +406,24 @@ sldg_status sldg_halo_widths(int64_t imin, int64_t imax, int64_t* left, int64_t*
     if (!left || !right || imin > imax) return fail(SLDG_EINVAL, "bad arguments");
     *left = std::max<int64_t>(0, imax + 1);
     *right = std::max<int64_t>(0, -imin);
+    return SLDG_OK;
+}
+
+sldg_status sldg_halo_plan(int64_t n, int world, int rank, int64_t pad, int64_t left, int64_t right,
+                           int64_t* out, int64_t max_entries, int64_t* n_entries)
+{
+    if (n < 1 || world < 1 || world > n || rank < 0 || rank >= world || left < 0 || right < 0 || !n_entries)
+        return fail(SLDG_EINVAL, "bad arguments");
+    std::vector<Xfer> xs = halo_plan(n, world, rank, pad, left, right);
+    *n_entries = (int64_t)xs.size();
+    if (!out) return SLDG_OK;
+    if ((int64_t)xs.size() > max_entries) return fail(SLDG_EINVAL, "output too small");
+    for (size_t i = 0; i < xs.size(); ++i) {
+        out[4 * i + 0] = xs[i].kind;
+        out[4 * i + 1] = xs[i].peer;
+        out[4 * i + 2] = xs[i].slot;
+        out[4 * i + 3] = xs[i].src;
+    }
     return SLDG_OK;
 }
 

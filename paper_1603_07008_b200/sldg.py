@@ -25,7 +25,7 @@ EXPORTS = [
     "sldg_advect_device", "sldg_mass", "sldg_shard_info", "sldg_sync", "sldg_set_stream",
     "sldg_get_stream", "sldg_memory_bytes", "sldg_last_error", "sldg_fill_random",
     "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
-    "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_layer_owner",
+    "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_halo_plan", "sldg_layer_owner",
 ]
 
 
@@ -80,6 +80,7 @@ def lib():
         "sldg_kernel_time": [vp, ctypes.c_int, dp, i64p, dp, ctypes.c_int],
         "sldg_nccl_unique_id": [vp],
         "sldg_halo_widths": [i64, i64, i64p, i64p],
+        "sldg_halo_plan": [i64, ctypes.c_int, ctypes.c_int, i64, i64, i64, i64p, i64, i64p],
         "sldg_layer_owner": [i64, ctypes.c_int, i64, ctypes.POINTER(ctypes.c_int), i64p],
     }
     for name, args in sig.items():
@@ -115,6 +116,15 @@ def halo_widths(imin: int, imax: int):
     a, b = ctypes.c_int64(), ctypes.c_int64()
     _check(lib().sldg_halo_widths(imin, imax, ctypes.byref(a), ctypes.byref(b)))
     return a.value, b.value
+
+
+def halo_plan(n: int, world: int, rank: int, pad: int, left: int, right: int):
+    """[(kind, peer, slot, src)] -- the transfer plan sldg_advect runs for a sharded sweep."""
+    cnt = ctypes.c_int64()
+    _check(lib().sldg_halo_plan(n, world, rank, pad, left, right, None, 0, ctypes.byref(cnt)))
+    buf = (ctypes.c_int64 * max(1, 4 * cnt.value))()
+    _check(lib().sldg_halo_plan(n, world, rank, pad, left, right, buf, cnt.value, ctypes.byref(cnt)))
+    return [tuple(buf[4 * i:4 * i + 4]) for i in range(cnt.value)]
 
 
 def layer_owner(n: int, world: int, layer: int):
