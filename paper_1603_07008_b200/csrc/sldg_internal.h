@@ -120,4 +120,20 @@ cudaError_t launch_field_range(const double* d_field, int64_t n, double shift, i
 
 constexpr int kMassBlocks = 592;  // 4 x 148 SMs; fixed => deterministic reduction order
 
+// ---- TMA-staged sweeps (sldg_sweep_tma.cu) ------------------------------------------------
+constexpr int kTmaConsumerWarps = 8;
+constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;  // + 1 producer warp
+struct TmaPlan {
+    int W = 0;      // strided: i_0 columns per tile
+    int T = 0;      // strided: targets along d per tile
+    int Rmax = 0;   // strided: source rows per slot per stage
+    int R = 0;      // d0: whole lines per stage
+    int GC = 0;     // d0: coupled groups per stage
+    int stage_bytes = 0;
+    int stages = 0;
+};
+bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl);
+cudaError_t launch_sweep_tma(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
+                             int64_t layer_begin, int64_t layer_end, const TmaPlan& pl, cudaStream_t s);
+
 }  // namespace sldg

@@ -21,6 +21,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
+
 #include <type_traits>
 
 #include "sldg_internal.h"
@@ -422,6 +424,15 @@ cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, 
                          int64_t layer_begin, int64_t layer_end, cudaStream_t s, int* n_launched)
 {
     *n_launched = (layer_end > layer_begin) ? 1 : 0;
+    // TMA-staged kernels when the shapes allow (sldg_sweep_tma.cu); SLDG_SWEEP=reg forces the
+    // register kernels below (A/B comparisons and tests of both paths).
+    static int mode = -1;
+    if (mode < 0) {
+        const char* e = getenv("SLDG_SWEEP");
+        mode = (e && e[0] == 'r') ? 0 : 1;
+    }
+    TmaPlan pl;
+    if (mode == 1 && tma_plan(lay, sw, &pl)) return launch_sweep_tma(lay, sw, src, dst, layer_begin, layer_end, pl, s);
     if (lay.prec == SLDG_FP64) return launch_sweep_p<SLDG_FP64>(lay, sw, src, dst, layer_begin, layer_end, s);
     return launch_sweep_p<SLDG_MIXED>(lay, sw, src, dst, layer_begin, layer_end, s);
 }
