@@ -203,9 +203,14 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweeps", default=None, help="comma list of dims to run (default: all)")
+    ap.add_argument("--dims", default=None, help="override grid extents (profiling slabs), e.g. 128,128,128,16")
     args = ap.parse_args()
 
     dims, kinds, k0, desc = CONFIGS[args.config]
+    if args.dims:
+        dims = [int(x) for x in args.dims.split(",")]
+        assert len(dims) == len(kinds)
+        desc = f"{desc} -- PROFILING SLAB dims={dims}"
     k = args.k or k0
     D, K = len(dims), k ** len(dims)
     cells = int(np.prod(dims))
