@@ -88,7 +88,12 @@ typedef struct {
     const void* nccl_unique_id; /* 128-byte ncclUniqueId, identical on all ranks, or NULL  */
     void* nccl_comm;            /* caller-owned ncclComm_t (rank/world must match), or NULL */
     int max_halo;               /* halo layers allocated per side; <= 0 selects 2          */
+    int flags;                  /* SLDG_DIST_* bits                                        */
 } sldg_dist;
+/* Run sweeps along the sharded dim through the halo path even when world == 1 (the ring
+ * neighbour is the rank itself: halo layers are device copies).  Exercises the exact halo
+ * addressing of multi-GPU runs on one GPU; no NCCL communicator is needed. */
+#define SLDG_DIST_FORCE_HALO 1
 
 /* Create a grid (zero-filled).  k in 1..SLDG_MAX_K coefficients per dim (the paper's order
  * o = p+1).  dist may be NULL (single GPU).  The device is the caller's current

@@ -24,6 +24,7 @@ struct sldg_grid_s : public Grid {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     int64_t* d_range = nullptr;
+    bool halo_mode = false;  // sweeps along the layer dim read halo layers (sharded, or forced)
 };
 
 namespace {
@@ -306,7 +307,7 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
         }
         n_entries = st;
     }
-    const bool sharded_sweep = (g->world > 1 && dim == L.D - 1);
+    const bool sharded_sweep = (g->halo_mode && dim == L.D - 1);
     int64_t imin = 0, imax = 0;
     if (!field) {
         if (!(fabs(shift) < 4.611686018427387904e18)) return fail(SLDG_EINVAL, "non-finite or huge shift");
@@ -494,7 +495,8 @@ sldg_status sldg_create(const sldg_grid_desc* grid, int k, const sldg_domain* do
         for (int d = 0; d < D - 1; ++d) L.L *= L.n[d];
         split(L.n[D - 1], world, rank, &L.first_layer, &L.layers);
     }
-    L.pad = (world > 1) ? ((dist->max_halo > 0) ? dist->max_halo : 2) : 0;
+    g->halo_mode = (world > 1) || (dist && (dist->flags & SLDG_DIST_FORCE_HALO) && D >= 2);
+    L.pad = g->halo_mode ? ((dist->max_halo > 0) ? dist->max_halo : 2) : 0;
     L.cells = L.layers * L.L;
     g->rank = rank;
     g->world = world;

@@ -126,6 +126,7 @@ constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;  // + 1 producer warp
 struct TmaPlan {
     int W = 0;      // strided: i_0 columns per tile
     int T = 0;      // strided: targets along d per tile
+    int Tsub = 0;   // strided: nominal targets per stage (rows = Rmax = Tsub + 4)
     int Rmax = 0;   // strided: source rows per slot per stage
     int R = 0;      // d0: whole lines per stage
     int GC = 0;     // d0: coupled groups per stage

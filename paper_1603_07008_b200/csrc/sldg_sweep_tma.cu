@@ -1,32 +1,43 @@
 // sldg_sweep_tma.cu -- TMA-staged SLDG sweep kernels for sm_100a.
 //
 // Same arithmetic as sldg_sweep.cu (readings R1-R6), different data movement:
-// a warp-specialised persistent kernel.  One producer warp streams the source rows of each
-// (tile, coupled group) into a ring of shared-memory stages with bulk asynchronous copies
-// (cp.async.bulk global->shared, completion counted on an mbarrier, SASS UBLKCP); the consumer
-// warps wait on the stage's "full" barrier, read their two source cells per target from
-// shared memory, do the fp64 contraction and write the outputs with coalesced streaming stores,
-// then release the stage on its "empty" barrier.  Bytes in flight are set by the number of
-// stages (~200 KB per SM), not by registers, which is what an HBM-bound stream needs.
+// a warp-specialised persistent kernel.  One producer thread streams the source rows of each
+// (tile, coupled group) into a ring of shared-memory stages with tensor TMA (one
+// cp.async.bulk.tensor box per coefficient slot per stage, SASS UTMALDG; completion counted on
+// an mbarrier); the consumer warps wait on the stage's "full" barrier, read their two source
+// cells per target from shared memory, do the fp64 contraction and write the outputs with
+// coalesced streaming stores, then release the stage on its "empty" barrier.  Bytes in flight
+// are set by the number of stages (~200 KB per SM), not by registers.
 //
-//   sweep_strided_tma  d >= 1: tile = W consecutive i_0 columns x T targets along d of one
-//                      perpendicular line set; per coupled group a stage holds the k slots'
-//                      rows [t0 - i*max - 1, t0 + T - 1 - i*min] (the union over the tile's
-//                      per-lane shifts), so per-lane CFL fields still read each row once.
-//                      Rows that are contiguous in HBM go in one copy.
+//   sweep_strided_tma  d >= 1: tile = W consecutive cells of the dims below d (the "lo" index,
+//                      contiguous in HBM) x a run of targets along d; per coupled group a stage
+//                      holds the k slots' rows [t0 - i*max - 1, t0 + te - 1 - i*min] (the union
+//                      over the tile's per-lane shifts), so per-lane CFL fields still read each
+//                      row once.  The rows of a stage are one run of consecutive source rows
+//                      (two when they wrap around the periodic line), each run loaded as boxes
+//                      of 2^h rows from a family of tensor maps (exact bytes, no over-fetch).
 //   sweep_d0_tma       d = 0: tile = R whole lines (the line is periodic, so the stage holds
 //                      every source cell and the modulo indexing is done in shared memory);
-//                      a stage holds GC coupled groups.
+//                      a stage holds GC coupled groups as one TMA box (+ one for the mass).
 // Consumers address HBM and shared memory by pointer increments set up once per stage; the
 // coupled group that holds the fp64 mass slot is a separate template instance.
+#include <cuda.h>  // CUtensorMap (types only; the encoder is fetched from the driver at run time)
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <string.h>
 
 #include <algorithm>
 
 #include "sldg_internal.h"
 
 namespace sldg {
+
+constexpr int kTmaHeights = 5;  // strided boxes of 1, 2, 4, 8, 16 rows (binary decomposition of a run)
+struct TmapSet {
+    CUtensorMap f[kTmaHeights];  // fp32 planes (mixed) or all slots (fp64)
+    CUtensorMap m[kTmaHeights];  // fp64 mass slot (mixed)
+};
 
 // ---- PTX helpers ----------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -60,8 +71,7 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
         "r"(parity)
         : "memory");
 }
-// bulk copy global -> shared, completion signalled as transaction bytes on `bar`;
-// evict-first L2 policy: every source byte is read once per sweep.
+// 1D bulk copy global -> shared (fallback for rows that wrap around a periodic line)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol)
 {
     asm volatile(
@@ -69,6 +79,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
             smem_u32(dst)),
         "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
         : "memory");
+}
+// 5D tensor box global -> shared (dense, row-major box in shared memory)
+__device__ __forceinline__ void tma_5d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, int c3, int c4,
+                                       uint64_t* bar, uint64_t pol)
+{
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)tm), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar)), "l"(pol)
+        : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm)
+{
+    asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)tm) : "memory");
 }
 __device__ __forceinline__ uint64_t policy_evict_first()
 {
@@ -109,38 +133,26 @@ __device__ __forceinline__ char* slot_ptr_w(const Arrays& a, const Layout& L, in
 {
     return const_cast<char*>(slot_ptr<PREC>(a, L, q, layerp, inner));
 }
-
-// element type of slot j of a coupled group
-template <int PREC, bool MASSG, int J>
-struct ET {
-    static constexpr bool dbl = (PREC == SLDG_FP64) || (MASSG && J == 0);
-};
 template <int PREC>
 __host__ __device__ __forceinline__ int esz_rt(bool massg, int j)
 {
     return (PREC == SLDG_FP64 || (massg && j == 0)) ? 8 : 4;
 }
-
 __device__ __forceinline__ void st_elem(char* p, int64_t i, double v, bool dbl)
 {
     if (dbl) __stcs(((double*)p) + i, v);
     else __stcs(((float*)p) + i, __double2float_rn(v));
 }
-__device__ __forceinline__ double ld_smem(const unsigned char* p, int i, bool dbl)
-{
-    return dbl ? ((const double*)p)[i] : (double)((const float*)p)[i];
-}
 
-// Strided consumer: one stage (one coupled group), one column, targets [lo, hi) of the sub-chunk.
+// Strided consumer: one stage (one coupled group), one column, `cnt` consecutive targets.
 // sb[j]: stage slot j at row 0 of this column; sstride: elements between rows; rB0: row of the
-// B-source of target lo; op[j]: output pointer of slot j at target lo; ostep: element step
-// between consecutive targets in each array (mass/fp64 vs fp32 planes).
+// B-source of the first target; op[j]: output pointer of slot j at the first target; ostep:
+// element step between consecutive targets (mass/fp64 array, fp32 planes).
 template <int KK, int PREC, bool MASSG>
 __device__ __forceinline__ void strided_consume(const unsigned char* const* sb, int sstride, int rB0, int cnt,
                                                 char* const* op, int64_t ostep_m, int64_t ostep_f, int cp,
                                                 const double* wr)
 {
-    // element j is fp64 for the fp64 variant and for the mass slot of the mass group
 #define SLDG_DBL(j) ((PREC == SLDG_FP64) || (MASSG && (j) == 0))
     const unsigned char* rp[KK];  // row pointers (advance one row per target)
     char* wp[KK];                 // output pointers (advance one target per target)
@@ -185,10 +197,16 @@ __device__ __forceinline__ void strided_consume(const unsigned char* const* sb, 
 
 // ============================================================================================
 // strided sweep (d >= 1)
+//   lo  = linear index over the dims below d (outer sweep: all dims below D-1), contiguous in
+//         HBM; a tile covers W consecutive lo values (its "columns")
+//   hi  = linear index over the dims strictly between d and D-1 (1 for the outer sweep)
+//   tensor maps (5D, fp32 planes or fp64 slots / fp64 mass):
+//         inner: {lo, i_d, hi, plane, layer}   outer: {lo, 1, 1, plane, layer}
 // ============================================================================================
 template <int KK, int PREC>
 __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Sweep sw, Arrays src, Arrays dst,
-                                                                  int64_t lb, int64_t le, TmaPlan pl)
+                                                                  int64_t lb, int64_t le, TmaPlan pl,
+                                                                  const __grid_constant__ TmapSet tmaps)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int S = pl.stages;
@@ -204,110 +222,98 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
             mbar_init(&empty[s], NC);
         }
         fence_barrier_init();
+        for (int h = 0; h < kTmaHeights; ++h) {
+            prefetch_tmap(&tmaps.f[h]);
+            if (PREC == SLDG_MIXED) prefetch_tmap(&tmaps.m[h]);
+        }
     }
     __syncthreads();
 
     const int D = lay.D, d = sw.dim;
     const bool outer = (d == D - 1);
-    const int W = pl.W, T = pl.T, Rmax = pl.Rmax;
-    const int64_t n0 = lay.n[0];
-    const int64_t nb0 = n0 / W;
+    const int W = pl.W, T = pl.T, Rmax = pl.Rmax, Tsub = pl.Tsub;
+    int64_t M_lo = 1, M_hi = 1;
+    for (int e = 0; e < (outer ? D - 1 : d); ++e) M_lo *= lay.n[e];
+    if (!outer)
+        for (int e = d + 1; e < D - 1; ++e) M_hi *= lay.n[e];
+    const int64_t nb = M_lo / W;
     const int64_t nlay = le - lb;
     const int64_t nline = outer ? nlay : sw.nd;
     const int64_t nseg = (nline + T - 1) / T;
-    int64_t nperp = 1;
-    for (int e = 1; e < D - 1; ++e)
-        if (e != d) nperp *= lay.n[e];
-    const int64_t ntiles = nseg * nb0 * nperp * (outer ? 1 : nlay);
+    const int64_t ntiles = nseg * nb * M_hi * (outer ? 1 : nlay);
     int kd = 1;
     for (int e = 0; e < d; ++e) kd *= KK;
     const int G = lay.K / KK;
-    const int64_t L = lay.L;
     const uint64_t pol = policy_evict_first();
     // element step between consecutive targets along d (mass/fp64 array, fp32 planes)
-    const int64_t tstep_m = outer ? (toff_m<PREC>(lay, 1, 0) - toff_m<PREC>(lay, 0, 0)) : lay.S[d];
-    const int64_t tstep_f = outer ? (toff_f<PREC>(lay, 1, 0) - toff_f<PREC>(lay, 0, 0)) : lay.S[d];
-    // rows of one slot are contiguous in HBM when the line stride equals the tile width
-    const bool rows_contig = !outer && lay.S[d] == W;
+    const int64_t tstep_m = outer ? (toff_m<PREC>(lay, 1, 0) - toff_m<PREC>(lay, 0, 0)) : M_lo;
+    const int64_t tstep_f = outer ? (toff_f<PREC>(lay, 1, 0) - toff_f<PREC>(lay, 0, 0)) : M_lo;
 
     const int NT = NC * 32;
     const int P = NT / W;
     const int tid = threadIdx.x;
     const int c = tid % W, part = tid / W;
 
-    uint32_t it = 0;  // stage-use counter, identical in every warp
-    // tile -> (segment along d, column block, perpendicular indices, layer)
-    auto decode = [&](int64_t tl, int64_t* idx, int64_t& cb, int64_t& layer, int64_t& inner_base, int64_t& t0) {
+    // tile -> (segment along d, column block, hi, layer)
+    auto decode = [&](int64_t tl, int64_t& cb, int64_t& hi, int64_t& layer, int64_t& t0) {
         int64_t rem = tl;
         const int64_t seg = rem % nseg;
         rem /= nseg;
-        cb = rem % nb0;
-        rem /= nb0;
-#pragma unroll
-        for (int e = 0; e < kMaxDim; ++e) idx[e] = 0;
-        for (int e = 1; e < D - 1; ++e)
-            if (e != d) {
-                idx[e] = rem % lay.n[e];
-                rem /= lay.n[e];
-            }
-        layer = 0;
-        if (!outer) {
-            layer = lb + rem;
-            idx[D - 1] = lay.first_layer + layer;
-        }
-        inner_base = cb * W;  // inner offset of the tile's column 0 at line coordinate 0
-        for (int e = 1; e < D - 1; ++e)
-            if (e != d) inner_base += idx[e] * lay.S[e];
+        cb = rem % nb;
+        rem /= nb;
+        hi = rem % M_hi;
+        rem /= M_hi;
+        layer = outer ? 0 : lb + rem;
         t0 = seg * T;
     };
-    auto findex = [&](const int64_t* idx, int64_t col) {
-        int64_t id2[kMaxDim];
+    // field entry of column lo (all perpendicular indices from lo, hi, layer)
+    auto findex = [&](int64_t lo, int64_t hi, int64_t layer) {
+        int64_t idx[kMaxDim];
 #pragma unroll
-        for (int e = 0; e < kMaxDim; ++e) id2[e] = idx[e];
-        id2[0] = col;
-        return tfield_index(sw, id2, D);
+        for (int e = 0; e < kMaxDim; ++e) idx[e] = 0;
+        const int elo = outer ? D - 1 : d;
+        for (int e = 0; e < elo; ++e) {
+            idx[e] = lo % lay.n[e];
+            lo /= lay.n[e];
+        }
+        if (!outer) {
+            for (int e = d + 1; e < D - 1; ++e) {
+                idx[e] = hi % lay.n[e];
+                hi /= lay.n[e];
+            }
+            idx[D - 1] = lay.first_layer + layer;
+        }
+        return tfield_index(sw, idx, D);
     };
     // The shifts of the NEXT tile's columns (for its shift span) are loaded while the current
-    // tile streams (software prefetch).  Tiles are whole lines where possible (tma_plan), so the
-    // per-tile consumer line data (A/B) is fetched once per ~k^{D-1} x n_d targets.
-    int64_t pf_sh[4];
+    // tile streams (software prefetch).
+    int64_t pf_sh[8];
     auto prefetch = [&](int64_t tl) {
-        int64_t idx[kMaxDim], cb, layer, inner_base, t0;
-        decode(tl, idx, cb, layer, inner_base, t0);
+        int64_t cb, hi, layer, t0;
+        decode(tl, cb, hi, layer, t0);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
             const int cc = lane + 32 * i;
-            pf_sh[i] = (cc < W) ? __ldg(&sw.shift[findex(idx, cb * W + cc)]) : 0;
+            pf_sh[i] = (cc < W) ? __ldg(&sw.shift[findex(cb * W + cc, hi, layer)]) : 0;
         }
     };
     if ((int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x);
 
+    uint32_t it = 0;  // stage-use counter, identical in every warp
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        int64_t idx[kMaxDim], cb, layer, inner_base, t0;
-        decode(tile, idx, cb, layer, inner_base, t0);
+        int64_t cb, hi, layer, t0;
+        decode(tile, cb, hi, layer, t0);
         const int nt = (int)((nline - t0) < T ? (nline - t0) : T);
         const int64_t tg0 = outer ? lay.first_layer + lb : 0;  // line coordinate of target index 0
+        const int64_t inner_base = outer ? cb * W : cb * W + hi * M_lo * sw.nd;  // column 0, coordinate 0
 
-        // shift range over the tile's W columns (every warp reduces its prefetched shifts)
         int64_t imin = INT64_MAX, imax = INT64_MIN;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < 8; ++i) {
             if (lane + 32 * i < W) {
                 imin = pf_sh[i] < imin ? pf_sh[i] : imin;
                 imax = pf_sh[i] > imax ? pf_sh[i] : imax;
             }
-        }
-        if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
-        // this tile's consumer line data: column shift, copy flag, A/B in registers
-        int64_t my_s = 0;
-        int my_cp = 0;
-        double wr[2 * KK * KK];
-        if (!producer) {
-            const int64_t f = findex(idx, cb * W + c);
-            my_s = __ldg(&sw.shift[f]);
-            my_cp = __ldg(&sw.copy[f]);
-#pragma unroll
-            for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
@@ -315,17 +321,16 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
             imin = a < imin ? a : imin;
             imax = b > imax ? b : imax;
         }
+        if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
         const int64_t span = imax - imin;
-        const int teff = (int)((Rmax - 1 - span) < nt ? (Rmax - 1 - span) : nt);
-        if (teff < 1) {
+        // sub-chunks of te targets: rows = te + 1 + span <= Rmax, balanced over the tile
+        const int tmax = (int)(Rmax - 1 - span);
+        (void)Tsub;
+        if (tmax < 1) {
             // ---- shift spread too wide for a stage: direct global loads (rare) ----
             if (!producer) {
                 for (int col = tid; col < W; col += NT) {
-                    int64_t id2[kMaxDim];
-#pragma unroll
-                    for (int e = 0; e < kMaxDim; ++e) id2[e] = idx[e];
-                    id2[0] = cb * W + col;
-                    const int64_t f = tfield_index(sw, id2, D);
+                    const int64_t f = findex(cb * W + col, hi, layer);
                     const int64_t s = __ldg(&sw.shift[f]);
                     const int cpf = __ldg(&sw.copy[f]);
                     const double* w = sw.ab + f * (2 * KK * KK);
@@ -343,16 +348,14 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
                             double va[KK], vb[KK];
                             for (int half = 0; half < 2; ++half) {
                                 int64_t x = xB - 1 + half, lp, in;
+                                int64_t xm = x % sw.nd;
+                                if (xm < 0) xm += sw.nd;
                                 if (outer) {
-                                    int64_t xm = x % sw.nd;
-                                    if (xm < 0) xm += sw.nd;
                                     lp = sw.wrap ? lay.pad + xm : x - lay.first_layer + lay.pad;
                                     in = inner_base + col;
                                 } else {
-                                    int64_t xm = x % sw.nd;
-                                    if (xm < 0) xm += sw.nd;
                                     lp = lay.pad + layer;
-                                    in = inner_base + col + xm * lay.S[d];
+                                    in = inner_base + col + xm * M_lo;
                                 }
 #pragma unroll
                                 for (int j = 0; j < KK; ++j) {
@@ -364,18 +367,15 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
                                 }
                             }
                             int64_t lp = outer ? lay.pad + lb + tt : lay.pad + layer;
-                            int64_t in = outer ? inner_base + col : inner_base + col + tt * lay.S[d];
+                            int64_t in = outer ? inner_base + col : inner_base + col + tt * M_lo;
 #pragma unroll
                             for (int j = 0; j < KK; ++j) {
                                 double o = 0.0;
-                                if (cpf) {
-                                    o = vb[j];
-                                } else {
 #pragma unroll
-                                    for (int l = 0; l < KK; ++l) o = fma(w[j * KK + l], va[l], o);
+                                for (int l = 0; l < KK; ++l) o = fma(w[j * KK + l], va[l], o);
 #pragma unroll
-                                    for (int l = 0; l < KK; ++l) o = fma(w[KK * KK + j * KK + l], vb[l], o);
-                                }
+                                for (int l = 0; l < KK; ++l) o = fma(w[KK * KK + j * KK + l], vb[l], o);
+                                o = cpf ? vb[j] : o;
                                 const int q = qbase + j * kd;
                                 st_elem(slot_ptr_w<PREC>(dst, lay, q, lp, in), 0, o, PREC == SLDG_FP64 || q == 0);
                             }
@@ -385,20 +385,43 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
             }
             continue;
         }
+        const int nsub = (nt + tmax - 1) / tmax;
+        const int tsz = (nt + nsub - 1) / nsub;
 
+        // this tile's consumer line data: column shift, copy flag, A/B in registers
+        int64_t my_s = 0;
+        int my_cp = 0;
+        double wr[2 * KK * KK];
+        if (!producer) {
+            const int64_t f = findex(cb * W + c, hi, layer);
+            my_s = __ldg(&sw.shift[f]);
+            my_cp = __ldg(&sw.copy[f]);
+#pragma unroll
+            for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
+        }
         // output position of target index 0 (padded layer, inner)
         const int64_t ob_lp = outer ? lay.pad + lb : lay.pad + layer;
         const int64_t ob_in = inner_base + c;
 
-        for (int sub = 0; sub < nt; sub += teff) {
-            const int te = (nt - sub) < teff ? (nt - sub) : teff;
+        for (int sub = 0; sub < nt; sub += tsz) {
+            const int te = (nt - sub) < tsz ? (nt - sub) : tsz;
             const int rows = te + 1 + (int)span;
             const int64_t rowbase = tg0 + t0 + sub - imax - 1;  // line coordinate of stage row 0
             // this consumer thread's targets [lo, hi) of the sub-chunk
             const int tp = (te + P - 1) / P;
-            const int lo = part * tp, hi = (lo + tp) < te ? (lo + tp) : te;
-            const int rB0 = (int)((tg0 + t0 + sub + lo - my_s) - rowbase);
-            const int64_t tl0 = t0 + sub + lo;  // local target index of `lo`
+            const int lo_t = part * tp, hi_t = (lo_t + tp) < te ? (lo_t + tp) : te;
+            const int rB0 = (int)((tg0 + t0 + sub + lo_t - my_s) - rowbase);
+            const int64_t tl0 = t0 + sub + lo_t;  // local target index of lo_t
+            // source row coordinate of stage row 0 in the tensor / memory
+            int64_t x0;
+            bool wraps = false;
+            if (sw.wrap) {
+                x0 = rowbase % sw.nd;
+                if (x0 < 0) x0 += sw.nd;
+                wraps = x0 + rows > sw.nd;
+            } else {
+                x0 = rowbase - lay.first_layer;  // local layer (halo rows live in the pad)
+            }
             for (int g = 0; g < G; ++g) {
                 const int s = it % S;
                 const uint32_t ph = (it / S) & 1;
@@ -417,46 +440,49 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
                 }
                 unsigned char* st = stage0 + (size_t)s * pl.stage_bytes;
                 if (producer) {
-                    if (lane == 0) mbar_wait(&empty[s], ph ^ 1);
-                    __syncwarp();
-                    uint32_t bytes = 0;
+                    if (lane == 0) {
+                        mbar_wait(&empty[s], ph ^ 1);
+                        uint32_t bytes = 0;
 #pragma unroll
-                    for (int j = 0; j < KK; ++j) bytes += (uint32_t)(rows * W * esz_rt<PREC>(massg, j));
-                    if (lane == 0) mbar_expect_tx(&full[s], bytes);
-                    __syncwarp();
-                    int64_t x0 = rowbase % sw.nd;  // wrapped coordinate of row 0 (wrap mode)
-                    if (x0 < 0) x0 += sw.nd;
-                    const bool one_copy = rows_contig && sw.wrap && (x0 + rows <= sw.nd);
-                    int soff = 0;
+                        for (int j = 0; j < KK; ++j) bytes += (uint32_t)(rows * W * esz_rt<PREC>(massg, j));
+                        mbar_expect_tx(&full[s], bytes);
+                        // the stage rows as runs of consecutive source rows (a new run each time
+                        // the rows wrap around the periodic line), each run as boxes of 2^h rows
+                        int soff = 0;
 #pragma unroll
-                    for (int j = 0; j < KK; ++j) {
-                        const int q = qbase + j * kd;
-                        const int es = esz_rt<PREC>(massg, j);
-                        const uint32_t rowb = (uint32_t)(W * es);
-                        if (one_copy) {
-                            if (lane == j)
-                                bulk_g2s(st + soff, slot_ptr<PREC>(src, lay, q, lay.pad + layer, inner_base + x0 * lay.S[d]),
-                                         rowb * rows, &full[s], pol);
-                        } else {
-                            for (int r = lane; r < rows; r += 32) {
-                                int64_t lp, in;
-                                if (sw.wrap) {
-                                    int64_t xm = x0 + r;
-                                    while (xm >= sw.nd) xm -= sw.nd;
-                                    lp = outer ? lay.pad + xm : lay.pad + layer;
-                                    in = outer ? inner_base : inner_base + xm * lay.S[d];
-                                } else {  // sharded layer dim: halo layers in the pad
-                                    lp = rowbase + r - lay.first_layer + lay.pad;
-                                    in = inner_base;
+                        for (int j = 0; j < KK; ++j) {
+                            const int q = qbase + j * kd;
+                            const bool mslot = (PREC == SLDG_MIXED) && q == 0;
+                            const int es = esz_rt<PREC>(massg, j);
+                            const int plane = (PREC == SLDG_FP64) ? q : (mslot ? 0 : q - 1);
+                            const CUtensorMap* tms = mslot ? tmaps.m : tmaps.f;
+                            int r = 0;        // next stage row
+                            int64_t x = x0;   // its source row coordinate
+                            while (r < rows) {
+                                int left = rows - r;  // rows in this run
+                                if (wraps && x + left > sw.nd) left = (int)(sw.nd - x);
+                                for (int h = kTmaHeights - 1; h >= 0; --h) {
+                                    while (left >= (1 << h)) {
+                                        unsigned char* dstp = st + soff + (size_t)r * W * es;
+                                        if (outer)
+                                            tma_5d(dstp, &tms[h], (int)(cb * W), 0, 0, plane, (int)(x + lay.pad), &full[s], pol);
+                                        else
+                                            tma_5d(dstp, &tms[h], (int)(cb * W), (int)x, (int)hi, plane,
+                                                   (int)(lay.pad + layer), &full[s], pol);
+                                        r += 1 << h;
+                                        x += 1 << h;
+                                        left -= 1 << h;
+                                    }
                                 }
-                                bulk_g2s(st + soff + r * rowb, slot_ptr<PREC>(src, lay, q, lp, in), rowb, &full[s], pol);
+                                if (wraps && x >= sw.nd) x -= sw.nd;
                             }
+                            soff += Rmax * W * es;
                         }
-                        soff += Rmax * W * es;
                     }
+                    __syncwarp();
                 } else {
                     mbar_wait(&full[s], ph);
-                    if (lo < hi) {
+                    if (lo_t < hi_t) {
                         const unsigned char* sb[KK];
                         char* op[KK];
                         int soff = 0;
@@ -470,9 +496,9 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
                                     (int64_t)tl0 * (es == 8 ? tstep_m * 8 : tstep_f * 4);
                         }
                         if (massg)
-                            strided_consume<KK, PREC, true>(sb, W, rB0, hi - lo, op, tstep_m, tstep_f, my_cp, wr);
+                            strided_consume<KK, PREC, true>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
                         else
-                            strided_consume<KK, PREC, false>(sb, W, rB0, hi - lo, op, tstep_m, tstep_f, my_cp, wr);
+                            strided_consume<KK, PREC, false>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
@@ -486,10 +512,9 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
 // contiguous sweep (d = 0): R whole lines x GC coupled groups per stage.  Every consumer thread
 // owns cells of ONE line of the tile (R = NT / n0 lines of one cell per thread when n0 <= NT,
 // else R = 1 and n0 / NT cells per thread), so its weights are loaded once per tile.
+//   tensor maps (5D): {box0, L / box0, 1, plane, layer}, box {box0, cs / box0, 1, BP, 1},
+//   cs = R n0 cells per stage row: one box = BP consecutive planes of the tile's cells.
 // ============================================================================================
-// one coupled group: sources at columns cA, cB of the k stage slots starting at `sp`
-// (slot stride cs elements), outputs to om (fp64 slot 0 of the mass group / fp64 variant) and
-// of (fp32 planes), each advanced by one plane (L elements) per slot.
 template <int KK, int PREC, bool MASSG>
 __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs, int cA, int cB, double*& om, float*& of,
                                          int64_t L, int cp, const double* wr)
@@ -528,7 +553,7 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs, int c
 }
 
 // all gc coupled groups of a stage for one target cell.  Mixed: om = mass of the cell, of =
-// plane of slot q0 (or q0+1 for the mass group); fp64: om = slot q0 of the cell.
+// plane of slot q0 (or of slot 1 for the mass group); fp64: om = slot q0 of the cell.
 template <int KK, int PREC, bool MASSG>
 __device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, int cs, int cA, int cB, double* om,
                                            float* of, int64_t L, int cp, const double* wr)
@@ -545,7 +570,8 @@ __device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, i
 
 template <int KK, int PREC>
 __global__ void __launch_bounds__(kTmaThreads) sweep_d0_tma(Layout lay, Sweep sw, Arrays src, Arrays dst, int64_t lb,
-                                                             int64_t le, TmaPlan pl)
+                                                             int64_t le, TmaPlan pl,
+                                                             const __grid_constant__ TmapSet tmaps)
 {
     extern __shared__ __align__(128) unsigned char smem[];
     const int S = pl.stages;
@@ -561,6 +587,10 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_d0_tma(Layout lay, Sweep sw
             mbar_init(&empty[s], NC);
         }
         fence_barrier_init();
+        for (int h = 0; h < kTmaHeights; ++h) {
+            prefetch_tmap(&tmaps.f[h]);
+            if (PREC == SLDG_MIXED) prefetch_tmap(&tmaps.m[h]);
+        }
     }
     __syncthreads();
 
@@ -575,6 +605,8 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_d0_tma(Layout lay, Sweep sw
     const int G = lay.K / KK;
     const int NT = NC * 32;
     const int cell_stride = R * n0;  // elements of one slot in a stage
+    const int box0 = pl.W;           // first box dim (cells)
+    const int BP = GC * KK;          // planes per box
     const uint64_t pol = policy_evict_first();
     // this thread's line of the tile and first cell
     const int my_r = (n0 <= NT) ? (int)threadIdx.x / n0 : 0;
@@ -631,19 +663,21 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_d0_tma(Layout lay, Sweep sw
             unsigned char* st = stage0 + (size_t)s * pl.stage_bytes;
             const bool massg = (PREC == SLDG_MIXED) && g0 == 0;
             if (producer) {
-                if (lane == 0) mbar_wait(&empty[s], ph ^ 1);
-                __syncwarp();
-                const int nslot = gc * KK;
-                const uint32_t bytes = (uint32_t)cell_stride * ((PREC == SLDG_FP64) ? 8u * nslot : 4u * nslot + (massg ? 4u : 0u));
-                if (lane == 0) mbar_expect_tx(&full[s], bytes);
-                __syncwarp();
-                for (int i = lane; i < nslot; i += 32) {
-                    const int q = g0 * KK + i;
-                    const int64_t soff = (PREC == SLDG_FP64) ? (int64_t)i * cell_stride * 8
-                                                             : (int64_t)i * cell_stride * 4 + ((massg && i > 0) ? (int64_t)cell_stride * 4 : 0);
-                    const uint32_t b = (uint32_t)cell_stride * ((PREC == SLDG_FP64 || q == 0) ? 8u : 4u);
-                    bulk_g2s(st + soff, slot_ptr<PREC>(src, lay, q, layerp, inner_base), b, &full[s], pol);
+                if (lane == 0) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    const uint32_t es = (PREC == SLDG_FP64) ? 8u : 4u;
+                    const uint32_t bytes = (uint32_t)cell_stride * (BP * es + (massg ? 8u : 0u));
+                    mbar_expect_tx(&full[s], bytes);
+                    const int c1 = (int)(inner_base / box0);
+                    if (massg) {
+                        tma_5d(st, &tmaps.m[0], 0, c1, 0, 0, (int)layerp, &full[s], pol);
+                        tma_5d(st + cell_stride * 8, &tmaps.f[0], 0, c1, 0, 0, (int)layerp, &full[s], pol);
+                    } else {
+                        const int plane0 = (PREC == SLDG_FP64) ? g0 * KK : g0 * KK - 1;
+                        tma_5d(st, &tmaps.f[0], 0, c1, 0, plane0, (int)layerp, &full[s], pol);
+                    }
                 }
+                __syncwarp();
             } else {
                 mbar_wait(&full[s], ph);
                 if (has_cell) {
@@ -678,7 +712,7 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_d0_tma(Layout lay, Sweep sw
 }
 
 // ============================================================================================
-// planning + launch
+// planning, tensor maps, launch
 // ============================================================================================
 static int g_num_sms = 0;
 static int g_smem_optin = 0;
@@ -692,10 +726,50 @@ static void query_device()
     cudaDeviceGetAttribute(&g_smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
 }
 
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encoder()
+{
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+// 5D tile tensor map; dims/strides in elements (stride[0] = 1 implied), box in elements
+static bool make_tmap(CUtensorMap* tm, bool f64, void* base, const int64_t* dims, const int64_t* strides,
+                      const int* box)
+{
+    EncodeTiledFn enc = encoder();
+    if (!enc) return false;
+    const int es = f64 ? 8 : 4;
+    cuuint64_t gd[5], gs[4];
+    cuuint32_t bd[5], estr[5] = {1, 1, 1, 1, 1};
+    for (int i = 0; i < 5; ++i) {
+        gd[i] = (cuuint64_t)dims[i];
+        bd[i] = (cuuint32_t)box[i];
+    }
+    for (int i = 0; i < 4; ++i) gs[i] = (cuuint64_t)strides[i + 1] * es;
+    CUresult r = enc(tm, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, base, gd, gs, bd,
+                     estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 // Returns true and fills `pl` when the TMA path applies to this sweep.
 bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
 {
     query_device();
+    if (!encoder()) return false;
     const int64_t n0 = lay.n[0];
     const int k = lay.k;
     const int64_t budget = std::min<int64_t>(g_smem_optin, 200 * 1024) - 256;
@@ -703,8 +777,10 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
     const int NT = kTmaConsumerWarps * 32;
     *pl = TmaPlan{};
     if (k > 4) return false;  // line weights live in registers; larger k uses the register kernels
+    if (n0 % 4 != 0) return false;
+    const int64_t layers_alloc = lay.layers + 2 * lay.pad;
+    if (lay.L > (int64_t)1 << 31 || layers_alloc > 65535) return false;
     if (sw.dim == 0) {
-        if (n0 % 4 != 0) return false;
         int64_t R;
         if (n0 <= NT) {
             if (NT % n0 != 0) return false;
@@ -715,50 +791,106 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
         }
         const int64_t lines = lay.L / n0;
         if (lines % R != 0) return false;
-        const int64_t group_bytes = R * n0 * bpc_max;  // one coupled group of the tile, worst case
+        const int64_t cs = R * n0;
+        const int64_t group_bytes = cs * bpc_max;  // one coupled group of the tile, worst case
         const int G = lay.K / k;
         const int64_t target = budget / 3;
         if (group_bytes > budget / 2) return false;
         int gcmax = (int)std::max<int64_t>(1, std::min<int64_t>(G, target / group_bytes));
         const int nchunk = (G + gcmax - 1) / gcmax;
         const int GC = (G + nchunk - 1) / nchunk;  // balanced chunks
+        if (GC * k > 256) return false;
         pl->R = (int)R;
         pl->GC = GC;
-        const int64_t slot_f = R * n0 * ((lay.prec == SLDG_FP64) ? 8 : 4);
-        pl->stage_bytes = (int)((GC * k * slot_f + ((lay.prec == SLDG_FP64) ? 0 : R * n0 * 4) + 127) / 128 * 128);
+        pl->W = (int)std::min<int64_t>(256, cs);  // first box dim
+        if (cs % pl->W != 0 || cs / pl->W > 256 || lay.L % pl->W != 0) return false;
+        const int es = (lay.prec == SLDG_FP64) ? 8 : 4;
+        // stage: [mass (mixed mass group)] + GC*k planes (the mass group's box holds one spare plane)
+        pl->stage_bytes = (int)((cs * (GC * k * es + ((lay.prec == SLDG_FP64) ? 0 : 8)) + 127) / 128 * 128);
         pl->stages = (int)std::min<int64_t>(8, budget / pl->stage_bytes);
         return pl->stages >= 2;
     }
-    int W = 0;
-    for (int w : {128, 64, 32})
-        if (n0 % w == 0) {
-            W = w;
-            break;
-        }
+    const bool outer = (sw.dim == lay.D - 1);
+    int64_t M_lo = 1;
+    for (int e = 0; e < (outer ? lay.D - 1 : sw.dim); ++e) M_lo *= lay.n[e];
+    // sub-chunk Tsub targets; stage rows Rmax = Tsub + 1 + 3 (shift spans up to 3 cells)
+    int W = 0, Tsub = 0;
+    const int Tsub0 = (k <= 3) ? 16 : 8;
+    for (int w : {256, 128, 64, 32}) {
+        if (M_lo % w != 0) continue;
+        int ts = Tsub0;
+        while (ts > 4 && (int64_t)(ts + 4) * w * bpc_max > budget / 3) ts /= 2;
+        if ((int64_t)(ts + 4) * w * bpc_max > budget / 2) continue;
+        W = w;
+        Tsub = ts;
+        break;
+    }
     if (W == 0) return false;
-    // sub-chunk: Tsub targets share a stage (rows = Tsub + 1 + shift span <= Rmax)
-    const int Tsub = (k <= 3) ? 16 : 8;
-    const int Rmax = Tsub + 1 + 3;
+    const int Rmax = Tsub + 4;
     const int64_t stage = (int64_t)Rmax * W * bpc_max;
     const int stage_bytes = (int)((stage + 127) / 128 * 128);
     const int stages = (int)std::min<int64_t>(8, budget / stage_bytes);
     if (stages < 2) return false;
     // tile length along d: whole lines (one line-data fetch per tile) unless that leaves fewer
     // than 4 tiles per SM, then the lines are cut into segments (multiples of Tsub)
-    const bool outer = (sw.dim == lay.D - 1);
     const int64_t nline = outer ? lay.layers : sw.nd;
-    int64_t base = (n0 / W) * (outer ? 1 : lay.layers);
-    for (int e = 1; e < lay.D - 1; ++e)
-        if (e != sw.dim) base *= lay.n[e];
+    int64_t base = (M_lo / W) * (outer ? 1 : lay.layers);
+    if (!outer)
+        for (int e = sw.dim + 1; e < lay.D - 1; ++e) base *= lay.n[e];
     const int64_t want = 4LL * g_num_sms;
     int64_t nseg = std::max<int64_t>(1, (want + base - 1) / base);
     int64_t T = (nline + nseg - 1) / nseg;
     T = std::max<int64_t>(Tsub, (T + Tsub - 1) / Tsub * Tsub);
     pl->W = W;
     pl->T = (int)T;
+    pl->Tsub = Tsub;
     pl->Rmax = Rmax;
     pl->stage_bytes = stage_bytes;
     pl->stages = stages;
+    return true;
+}
+
+// tensor maps of the source array for a sweep.  d0: one box shape (index 0).  Strided: box
+// heights 2^h rows, h = 0..kTmaHeights-1 (index h).
+static bool build_tmaps(const Layout& lay, const Sweep& sw, const Arrays& src, const TmaPlan& pl, TmapSet* ts)
+{
+    const bool f64 = lay.prec == SLDG_FP64;
+    const int64_t P = f64 ? lay.K : lay.K - 1;  // planes in the fp32 (or fp64) array
+    const int64_t layers_alloc = lay.layers + 2 * lay.pad;
+    const int64_t L = lay.L;
+    void* fbase = f64 ? (void*)src.s64 : (void*)src.pl;
+    if (sw.dim == 0) {
+        const int64_t b0 = pl.W, cs = (int64_t)pl.R * lay.n[0];
+        const int64_t dm[5] = {b0, L / b0, 1, P, layers_alloc};
+        const int64_t sm[5] = {1, b0, L, L, L * P};
+        const int bx[5] = {(int)b0, (int)(cs / b0), 1, pl.GC * lay.k, 1};
+        if (!make_tmap(&ts->f[0], f64, fbase, dm, sm, bx)) return false;
+        if (!f64) {
+            const int64_t dmm[5] = {b0, L / b0, 1, 1, layers_alloc};
+            const int64_t smm[5] = {1, b0, L, L, L};
+            const int bxm[5] = {(int)b0, (int)(cs / b0), 1, 1, 1};
+            if (!make_tmap(&ts->m[0], true, src.mass, dmm, smm, bxm)) return false;
+        }
+        return true;
+    }
+    const bool outer = (sw.dim == lay.D - 1);
+    int64_t M_lo = 1, M_hi = 1;
+    for (int e = 0; e < (outer ? lay.D - 1 : sw.dim); ++e) M_lo *= lay.n[e];
+    if (!outer)
+        for (int e = sw.dim + 1; e < lay.D - 1; ++e) M_hi *= lay.n[e];
+    const int64_t nd = outer ? 1 : sw.nd;
+    for (int h = 0; h < kTmaHeights; ++h) {
+        const int rowsb = 1 << h;
+        const int64_t dm[5] = {M_lo, nd, M_hi, P, layers_alloc};
+        const int64_t sm[5] = {1, M_lo, M_lo * nd, L, L * P};
+        const int bx[5] = {pl.W, outer ? 1 : rowsb, 1, 1, outer ? rowsb : 1};
+        if (!make_tmap(&ts->f[h], f64, fbase, dm, sm, bx)) return false;
+        if (!f64) {
+            const int64_t dmm[5] = {M_lo, nd, M_hi, 1, layers_alloc};
+            const int64_t smm[5] = {1, M_lo, M_lo * nd, L, L};
+            if (!make_tmap(&ts->m[h], true, src.mass, dmm, smm, bx)) return false;
+        }
+    }
     return true;
 }
 
@@ -766,6 +898,9 @@ template <int KK, int PREC>
 static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst, int64_t lb,
                                 int64_t le, const TmaPlan& pl, cudaStream_t s)
 {
+    TmapSet tmaps;
+    memset(&tmaps, 0, sizeof(tmaps));
+    if (!build_tmaps(lay, sw, src, pl, &tmaps)) return cudaErrorInvalidValue;
     const size_t smem = 256 + (size_t)pl.stages * pl.stage_bytes;
     int64_t ntiles;
     const int per_sm = std::max<int>(1, (int)(228 * 1024 / (smem + 1024)));
@@ -775,19 +910,20 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
-        kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl);
+        kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
     } else {
         const bool outer = (sw.dim == lay.D - 1);
         const int64_t nline = outer ? (le - lb) : sw.nd;
-        int64_t nperp = 1;
-        for (int e = 1; e < lay.D - 1; ++e)
-            if (e != sw.dim) nperp *= lay.n[e];
-        ntiles = ((nline + pl.T - 1) / pl.T) * (lay.n[0] / pl.W) * nperp * (outer ? 1 : (le - lb));
+        int64_t M_lo = 1, M_hi = 1;
+        for (int e = 0; e < (outer ? lay.D - 1 : sw.dim); ++e) M_lo *= lay.n[e];
+        if (!outer)
+            for (int e = sw.dim + 1; e < lay.D - 1; ++e) M_hi *= lay.n[e];
+        ntiles = ((nline + pl.T - 1) / pl.T) * (M_lo / pl.W) * M_hi * (outer ? 1 : (le - lb));
         auto kern = sweep_strided_tma<KK, PREC>;
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
-        kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl);
+        kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
     }
     return cudaGetLastError();
 }

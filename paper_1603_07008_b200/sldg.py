@@ -45,7 +45,9 @@ class Domain(ctypes.Structure):
 
 class Dist(ctypes.Structure):
     _fields_ = [("rank", ctypes.c_int), ("world", ctypes.c_int), ("nccl_unique_id", ctypes.c_void_p),
-                ("nccl_comm", ctypes.c_void_p), ("max_halo", ctypes.c_int)]
+                ("nccl_comm", ctypes.c_void_p), ("max_halo", ctypes.c_int), ("flags", ctypes.c_int)]
+
+SLDG_DIST_FORCE_HALO = 1
 
 
 _lib = None
@@ -137,7 +139,8 @@ class Grid:
     """Owns one sldg_grid handle.  Method names follow the C ABI (sldg_<name>)."""
 
     def __init__(self, cells, k: int, lo=None, hi=None, precision: str = "mixed",
-                 rank: int = 0, world: int = 1, unique_id: bytes | None = None, max_halo: int = 0):
+                 rank: int = 0, world: int = 1, unique_id: bytes | None = None, max_halo: int = 0,
+                 force_halo: bool = False):
         cells = [int(c) for c in cells]
         self.D = len(cells)
         self.cells = cells
@@ -152,10 +155,13 @@ class Grid:
         prec = {"mixed": SLDG_MIXED, "fp64": SLDG_FP64}[precision]
         dist_p = None
         self._uid = None
-        if world > 1:
-            self._uid = ctypes.create_string_buffer(unique_id, 128)
-            dist = Dist(rank, world, ctypes.cast(self._uid, ctypes.c_void_p), None, max_halo)
-            dist_p = ctypes.byref(dist)
+        if world > 1 or force_halo:
+            uid = None
+            if world > 1:
+                self._uid = ctypes.create_string_buffer(unique_id, 128)
+                uid = ctypes.cast(self._uid, ctypes.c_void_p)
+            self._dist = Dist(rank, world, uid, None, max_halo, SLDG_DIST_FORCE_HALO if force_halo else 0)
+            dist_p = ctypes.byref(self._dist)
         h = ctypes.c_void_p()
         _check(lib().sldg_create(ctypes.byref(gd), self.k, ctypes.byref(dom), prec, dist_p, ctypes.byref(h)))
         self.h = h

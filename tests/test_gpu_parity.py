@@ -378,3 +378,30 @@ def test_c5_full_size_sampled_lines():
         g.advect(d, field=f, field_mask=mask)
         _sampled_line_parity(g, dims, k, "mixed", d, f, mask, 1603, 3, rng)
     g.destroy()
+
+
+# ------------------------------------------------------------------------------ halo path (1 GPU)
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+@pytest.mark.parametrize("dims,k", [([64, 24], 3), ([32, 6, 20], 2), ([128, 4, 3, 18], 3), ([16, 8, 8, 9], 4)])
+def test_forced_halo_path_matches_oracle(dims, k, precision):
+    """The multi-GPU halo addressing (pad layers, halo exchange plan, interior/boundary launch
+    split) run on one GPU: SLDG_DIST_FORCE_HALO makes the rank its own ring neighbour.  Every
+    dim is swept (pad > 0 changes every kernel's addressing); the layer-dim sweeps use shifts
+    up to the halo width and a per-lane field."""
+    from paper_1603_07008_b200 import SldgError
+    D, K = len(dims), k ** len(dims)
+    c = sldg_inputs.random_coeffs(dims, k, 4242)
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision, force_halo=True, max_halo=3)
+    rng = np.random.default_rng(len(dims))
+    cases = [(d, 1.37, None, 0) for d in range(D)]
+    cases += [(D - 1, -2.25, None, 0), (D - 1, 2.0, None, 0), (D - 1, 0.0, rng.uniform(-2.9, 1.9, dims[0]), 1)]
+    for d, shift, field, mask in cases:
+        g.set_coeffs(c)
+        g.advect(d, shift=shift, field=field, field_mask=mask)
+        ref = oracle.advect(ref_in, dims, k, d, shift=shift, field=field, field_mask=mask,
+                            n_double=n_double(precision, K))
+        assert_parity(g.get_coeffs(), ref, K, precision, f"halo dims={dims} dim={d} nu={shift}", ref_in, d, k)
+    with pytest.raises(SldgError):  # halo of 5 layers > max_halo = 3
+        g.advect(D - 1, shift=4.5)
+    g.destroy()
