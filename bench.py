@@ -199,7 +199,7 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--eps", type=float, default=0.01)
     ap.add_argument("--ref-lines", type=int, default=2048)
-    ap.add_argument("--cpu-lines", type=int, default=12000)
+    ap.add_argument("--cpu-lines", type=int, default=6000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--sweeps", default=None, help="comma list of dims to run (default: all)")

@@ -94,6 +94,12 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* tm)
 {
     asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)tm) : "memory");
 }
+__device__ __forceinline__ uint64_t policy_evict_normal()
+{
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first()
 {
     uint64_t p;
@@ -164,11 +170,36 @@ __device__ __forceinline__ void strided_consume(const unsigned char* const* sb, 
         wstep[j] = SLDG_DBL(j) ? ostep_m * 8 : ostep_f * 4;
     }
     const int rstep = sstride;  // elements
-    double va[KK], vb[KK];
+    if (cp) {  // alpha == 0: exact copy of the B-source, bit for bit (R4); rare, so a branch
+        for (int u = 0; u < cnt; ++u) {
 #pragma unroll
-    for (int j = 0; j < KK; ++j) {
-        va[j] = SLDG_DBL(j) ? *(const double*)rp[j] : (double)*(const float*)rp[j];
-        rp[j] += rstep * (SLDG_DBL(j) ? 8 : 4);
+            for (int j = 0; j < KK; ++j) {
+                rp[j] += rstep * (SLDG_DBL(j) ? 8 : 4);
+                if (SLDG_DBL(j)) __stcs((double*)wp[j], *(const double*)rp[j]);
+                else __stcs((float*)wp[j], *(const float*)rp[j]);
+                wp[j] += wstep[j];
+            }
+        }
+        return;
+    }
+    // o_j(t) = sum_l A_jl a_l(t) + sum_l B_jl b_l(t) with a(t+1) = b(t): the A-part of target
+    // t+1 is accumulated from the row just loaded for target t, so each output's dependent FMA
+    // chain is k long instead of 2k (same operation order, hence the same rounding).
+    double sA[KK], vb[KK];
+    {
+        double va[KK];
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            va[j] = SLDG_DBL(j) ? *(const double*)rp[j] : (double)*(const float*)rp[j];
+            rp[j] += rstep * (SLDG_DBL(j) ? 8 : 4);
+        }
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < KK; ++l) s = fma(wr[j * KK + l], va[l], s);
+            sA[j] = s;
+        }
     }
 #pragma unroll 2
     for (int u = 0; u < cnt; ++u) {
@@ -179,18 +210,20 @@ __device__ __forceinline__ void strided_consume(const unsigned char* const* sb, 
         }
 #pragma unroll
         for (int j = 0; j < KK; ++j) {
-            double o = 0.0;
-#pragma unroll
-            for (int l = 0; l < KK; ++l) o = fma(wr[j * KK + l], va[l], o);
+            double o = sA[j];
 #pragma unroll
             for (int l = 0; l < KK; ++l) o = fma(wr[KK * KK + j * KK + l], vb[l], o);
-            o = cp ? vb[j] : o;  // alpha == 0: exact copy (R4)
             if (SLDG_DBL(j)) __stcs((double*)wp[j], o);
             else __stcs((float*)wp[j], __double2float_rn(o));
             wp[j] += wstep[j];
         }
 #pragma unroll
-        for (int j = 0; j < KK; ++j) va[j] = vb[j];
+        for (int j = 0; j < KK; ++j) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < KK; ++l) s = fma(wr[j * KK + l], vb[l], s);
+            sA[j] = s;
+        }
     }
 #undef SLDG_DBL
 }
@@ -244,7 +277,8 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
     int kd = 1;
     for (int e = 0; e < d; ++e) kd *= KK;
     const int G = lay.K / KK;
-    const uint64_t pol = policy_evict_first();
+    // default L2 priority: the last rows of a sub-chunk are read again by the next one
+    const uint64_t pol = policy_evict_normal();
     // element step between consecutive targets along d (mass/fp64 array, fp32 planes)
     const int64_t tstep_m = outer ? (toff_m<PREC>(lay, 1, 0) - toff_m<PREC>(lay, 0, 0)) : M_lo;
     const int64_t tstep_f = outer ? (toff_f<PREC>(lay, 1, 0) - toff_f<PREC>(lay, 0, 0)) : M_lo;
@@ -540,7 +574,7 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs, int c
         for (int l = 0; l < KK; ++l) o = fma(wr[j * KK + l], va[l], o);
 #pragma unroll
         for (int l = 0; l < KK; ++l) o = fma(wr[KK * KK + j * KK + l], vb[l], o);
-        o = cp ? vb[j] : o;  // alpha == 0: exact copy (R4)
+        if (cp) o = vb[j];  // alpha == 0: exact copy (R4); fp32 -> fp64 -> fp32 round trip is exact
         if (SLDG_DBL(j)) {
             __stcs(om, o);
             om += L;
@@ -564,8 +598,12 @@ __device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, i
         d0_group<KK, PREC, true>(sp, cs, cA, cB, om, of, L, cp, wr);
         gi = 1;
     }
-#pragma unroll 1
-    for (; gi < gc; ++gi) d0_group<KK, PREC, false>(sp, cs, cA, cB, om, of, L, cp, wr);
+    // two groups per iteration: independent FMA chains for the scheduler to interleave
+    for (; gi + 1 < gc; gi += 2) {
+        d0_group<KK, PREC, false>(sp, cs, cA, cB, om, of, L, cp, wr);
+        d0_group<KK, PREC, false>(sp, cs, cA, cB, om, of, L, cp, wr);
+    }
+    if (gi < gc) d0_group<KK, PREC, false>(sp, cs, cA, cB, om, of, L, cp, wr);
 }
 
 template <int KK, int PREC>
