@@ -202,6 +202,8 @@ def main():
     ap.add_argument("--cpu-lines", type=int, default=6000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--compare-fp64", action=argparse.BooleanOptionalAction, default=True,
+                    help="also time the all-fp64 layout on a slab of the workload (mixed_vs_fp64)")
     ap.add_argument("--sweeps", default=None, help="comma list of dims to run (default: all)")
     ap.add_argument("--dims", default=None, help="override grid extents (profiling slabs), e.g. 128,128,128,16")
     args = ap.parse_args()
@@ -349,7 +351,7 @@ def main():
             "hbm_frac_of_peak": alg_bytes_step / (step_ms * 1e-3) / 1e9 / world / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
-                         "kernel": f"sweep along dim {dom} ({'sweep_d0_kernel' if dom == 0 else 'sweep_strided_kernel'})",
+                         "kernel": f"{g.sweep_kernel(dom)} (sweep along dim {dom})",
                          "peak_source": peak_src,
                          "bytes_per_launch": d_bytes / d_n if d_n else None,
                          "avg_launch_ms": d_ms / d_n if d_n else None},
@@ -363,11 +365,58 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
-        print(json.dumps(out))
     g.destroy()
+    del dev_fields
+    if rank == 0:
+        if args.compare_fp64 and world == 1:
+            out["mixed_vs_fp64"] = compare_precisions(args, dims, kinds, k)
+        print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def compare_precisions(args, dims, kinds, k):
+    """North_star 'mixed >= 1.6x faster than all-fp64': the same split step on both storage
+    layouts, on a slab of the workload small enough that the fp64 pair fits one GPU (the outer
+    dim cut to 32 layers).  Device time over the same sweeps, CUDA events on the grid stream."""
+    import torch
+
+    from paper_1603_07008_b200 import Grid
+
+    sdims = list(dims)
+    if int(np.prod(sdims)) * 8 * k ** len(dims) * 2 > 120e9:
+        sdims[-1] = 32
+    lo, hi = domain(kinds)
+    res = {"slab_dims": sdims}
+    for prec in ["mixed", "fp64"]:
+        g = Grid(sdims, k, lo=lo, hi=hi, precision=prec)
+        g.fill_separable(sldg_inputs.landau_terms(sdims, k, kinds, lo, hi, eps=args.eps))
+        sweeps = sldg_inputs.vlasov_fields(sdims, kinds, lo, hi, eps=args.eps)
+        dfs = [torch.tensor(f, dtype=torch.float64, device="cuda") for _, f, _ in sweeps]
+        torch.cuda.synchronize()
+        stream = torch.cuda.ExternalStream(g.stream())
+        for _ in range(2):
+            for (d, _, m), tf in zip(sweeps, dfs):
+                g.advect_device(d, tf.data_ptr(), m)
+        g.sync()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(stream):
+            e0.record(stream)
+        for _ in range(3):
+            for (d, _, m), tf in zip(sweeps, dfs):
+                g.advect_device(d, tf.data_ptr(), m)
+        with torch.cuda.stream(stream):
+            e1.record(stream)
+        g.sync()
+        res[f"{prec}_ms_per_step"] = e0.elapsed_time(e1) / 3
+        g.destroy()
+        del dfs
+        torch.cuda.synchronize()
+    res["speedup"] = res["fp64_ms_per_step"] / res["mixed_ms_per_step"]
+    K = k ** len(dims)
+    res["memorydown"] = bytes_per_cell(K, "fp64") / bytes_per_cell(K, "mixed")
+    return res
 
 
 if __name__ == "__main__":

@@ -158,6 +158,10 @@ sldg_status sldg_profile(sldg_grid g, int enable);
 sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches, double* bytes, int reset);
 /* Number of kernels this handle has launched (all kinds). */
 int64_t sldg_launch_count(sldg_grid g);
+/* Name of the sweep kernel a sweep along `dim` uses on this grid (static string; "" on bad
+ * arguments): the TMA-staged kernels when their shape constraints hold, else the register
+ * kernels. */
+const char* sldg_sweep_kernel(sldg_grid g, int dim);
 
 /* ---- distributed helpers ---------------------------------------------------------------- */
 /* Write a fresh 128-byte ncclUniqueId into out128 (call on rank 0, broadcast it). */

@@ -780,4 +780,13 @@ sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches
 
 int64_t sldg_launch_count(sldg_grid g) { return g ? g->launches : 0; }
 
+const char* sldg_sweep_kernel(sldg_grid g, int dim)
+{
+    if (!g || dim < 0 || dim >= g->lay.D) return "";
+    Sweep sw{};
+    sw.dim = dim;
+    sw.nd = g->lay.n[dim];
+    return sweep_kernel_name(g->lay, sw);
+}
+
 }  // extern "C"

@@ -134,6 +134,7 @@ struct TmaPlan {
     int stages = 0;
 };
 bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl);
+const char* sweep_kernel_name(const Layout& lay, const Sweep& sw);
 cudaError_t launch_sweep_tma(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
                              int64_t layer_begin, int64_t layer_end, const TmaPlan& pl, cudaStream_t s);
 

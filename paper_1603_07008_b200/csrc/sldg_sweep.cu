@@ -420,6 +420,15 @@ static cudaError_t launch_sweep_p(const Layout& lay, const Sweep& sw, const Arra
     return cudaErrorInvalidValue;
 }
 
+const char* sweep_kernel_name(const Layout& lay, const Sweep& sw)
+{
+    const char* e = getenv("SLDG_SWEEP");
+    TmaPlan pl;
+    const bool tma = !(e && e[0] == 'r') && tma_plan(lay, sw, &pl);
+    if (sw.dim == 0) return tma ? "sweep_d0_tma" : "sweep_d0_kernel";
+    return tma ? "sweep_strided_tma" : "sweep_strided_kernel";
+}
+
 cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
                          int64_t layer_begin, int64_t layer_end, cudaStream_t s, int* n_launched)
 {

@@ -25,9 +25,11 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
+#include <mutex>
 
 #include "sldg_internal.h"
 
@@ -832,7 +834,9 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
         const int64_t cs = R * n0;
         const int64_t group_bytes = cs * bpc_max;  // one coupled group of the tile, worst case
         const int G = lay.K / k;
-        const int64_t target = budget / 3;
+        int64_t d0div = 3;  // stage <= budget / d0div (tuning override SLDG_TMA_D0DIV)
+        if (const char* e = getenv("SLDG_TMA_D0DIV")) d0div = atoi(e);
+        const int64_t target = budget / d0div;
         if (group_bytes > budget / 2) return false;
         int gcmax = (int)std::max<int64_t>(1, std::min<int64_t>(G, target / group_bytes));
         const int nchunk = (G + gcmax - 1) / gcmax;
@@ -853,12 +857,19 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
     for (int e = 0; e < (outer ? lay.D - 1 : sw.dim); ++e) M_lo *= lay.n[e];
     // sub-chunk Tsub targets; stage rows Rmax = Tsub + 1 + 3 (shift spans up to 3 cells)
     int W = 0, Tsub = 0;
-    const int Tsub0 = (k <= 3) ? 16 : 8;
+    // Measured on B200 (tools/tune_tma.sh, profiles/round1/tuning.md): few LARGE stages beat many
+    // small ones -- per-stage consumer overhead (barrier round trip, pointer setup, the A-part
+    // prologue row) is amortised over more targets.  Default: 2 stages, Tsub as large as fits.
+    int Tsub0 = 64;
+    int Wmax = 256;
+    int64_t sdiv = 2;  // stage <= budget / sdiv
+    if (const char* e = getenv("SLDG_TMA_W")) Wmax = atoi(e);        // tuning overrides
+    if (const char* e = getenv("SLDG_TMA_TSUB")) Tsub0 = atoi(e);
+    if (const char* e = getenv("SLDG_TMA_SDIV")) sdiv = atoi(e);
     for (int w : {256, 128, 64, 32}) {
-        if (M_lo % w != 0) continue;
-        int ts = Tsub0;
-        while (ts > 4 && (int64_t)(ts + 4) * w * bpc_max > budget / 3) ts /= 2;
-        if ((int64_t)(ts + 4) * w * bpc_max > budget / 2) continue;
+        if (M_lo % w != 0 || w > Wmax) continue;
+        int ts = (int)std::min<int64_t>(Tsub0, budget / sdiv / ((int64_t)w * bpc_max) - 4);
+        if (ts < 4) continue;
         W = w;
         Tsub = ts;
         break;
@@ -932,20 +943,75 @@ static bool build_tmaps(const Layout& lay, const Sweep& sw, const Arrays& src, c
     return true;
 }
 
+// Encoding 10 tensor maps costs tens of microseconds of host time per sweep, which matters for
+// small grids; the maps only depend on the source buffer, the layout and the plan, so they are
+// cached (two ping-pong buffers x D dims per grid; mutex-protected, handles may live on
+// different threads).
+struct TmapCacheEntry {
+    bool valid = false;
+    const void* f = nullptr;
+    const void* m = nullptr;
+    int dim = 0, W = 0, T = 0, Rmax = 0, R = 0, GC = 0;
+    int64_t L = 0, layers = 0, pad = 0, nd = 0, K = 0;
+    TmapSet maps;
+};
+
+static bool cached_tmaps(const Layout& lay, const Sweep& sw, const Arrays& src, const TmaPlan& pl, TmapSet* out)
+{
+    static std::mutex mu;
+    static TmapCacheEntry cache[32];
+    static int next = 0;
+    const void* f = lay.prec == SLDG_FP64 ? (const void*)src.s64 : (const void*)src.pl;
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : cache)
+        if (e.valid && e.f == f && e.m == src.mass && e.dim == sw.dim && e.W == pl.W && e.T == pl.T &&
+            e.Rmax == pl.Rmax && e.R == pl.R && e.GC == pl.GC && e.L == lay.L && e.layers == lay.layers &&
+            e.pad == lay.pad && e.nd == sw.nd && e.K == lay.K) {
+            *out = e.maps;
+            return true;
+        }
+    TmapCacheEntry& e = cache[next];
+    next = (next + 1) % 32;
+    memset(&e.maps, 0, sizeof(e.maps));
+    if (!build_tmaps(lay, sw, src, pl, &e.maps)) {
+        e.valid = false;
+        return false;
+    }
+    e.valid = true;
+    e.f = f;
+    e.m = src.mass;
+    e.dim = sw.dim;
+    e.W = pl.W;
+    e.T = pl.T;
+    e.Rmax = pl.Rmax;
+    e.R = pl.R;
+    e.GC = pl.GC;
+    e.L = lay.L;
+    e.layers = lay.layers;
+    e.pad = lay.pad;
+    e.nd = sw.nd;
+    e.K = lay.K;
+    *out = e.maps;
+    return true;
+}
+
 template <int KK, int PREC>
 static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst, int64_t lb,
                                 int64_t le, const TmaPlan& pl, cudaStream_t s)
 {
     TmapSet tmaps;
-    memset(&tmaps, 0, sizeof(tmaps));
-    if (!build_tmaps(lay, sw, src, pl, &tmaps)) return cudaErrorInvalidValue;
+    if (!cached_tmaps(lay, sw, src, pl, &tmaps)) return cudaErrorInvalidValue;
     const size_t smem = 256 + (size_t)pl.stages * pl.stage_bytes;
     int64_t ntiles;
     const int per_sm = std::max<int>(1, (int)(228 * 1024 / (smem + 1024)));
     if (sw.dim == 0) {
         ntiles = (lay.L / lay.n[0] / pl.R) * (le - lb);
         auto kern = sweep_d0_tma<KK, PREC>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        static bool attr_set = false;  // once per instantiation: allow the full opt-in carveout
+        if (!attr_set) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
+            attr_set = true;
+        }
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
@@ -958,7 +1024,11 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
             for (int e = sw.dim + 1; e < lay.D - 1; ++e) M_hi *= lay.n[e];
         ntiles = ((nline + pl.T - 1) / pl.T) * (M_lo / pl.W) * M_hi * (outer ? 1 : (le - lb));
         auto kern = sweep_strided_tma<KK, PREC>;
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        static bool attr_set = false;  // once per instantiation: allow the full opt-in carveout
+        if (!attr_set) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
+            attr_set = true;
+        }
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);

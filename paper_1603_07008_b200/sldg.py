@@ -26,6 +26,7 @@ EXPORTS = [
     "sldg_get_stream", "sldg_memory_bytes", "sldg_last_error", "sldg_fill_random",
     "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
     "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_halo_plan", "sldg_layer_owner",
+    "sldg_sweep_kernel",
 ]
 
 
@@ -95,6 +96,8 @@ def lib():
     L.sldg_last_error.restype = ctypes.c_char_p
     L.sldg_launch_count.argtypes = [vp]
     L.sldg_launch_count.restype = ctypes.c_int64
+    L.sldg_sweep_kernel.argtypes = [vp, ctypes.c_int]
+    L.sldg_sweep_kernel.restype = ctypes.c_char_p
     _lib = L
     return L
 
@@ -250,3 +253,6 @@ class Grid:
 
     def launch_count(self) -> int:
         return int(lib().sldg_launch_count(self.h))
+
+    def sweep_kernel(self, dim: int) -> str:
+        return lib().sldg_sweep_kernel(self.h, int(dim)).decode()
