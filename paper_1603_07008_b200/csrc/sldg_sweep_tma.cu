@@ -551,11 +551,30 @@ __global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Swe
 //   tensor maps (5D): {box0, L / box0, 1, plane, layer}, box {box0, cs / box0, 1, BP, 1},
 //   cs = R n0 cells per stage row: one box = BP consecutive planes of the tile's cells.
 // ============================================================================================
-template <int KK, int PREC, bool MASSG>
-__device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs, int cA, int cB, double*& om, float*& of,
-                                         int64_t L, int cp, const double* wr)
+// One coupled group.  sa / sb: the stage bytes of this cell's A- and B-source columns in the
+// group's first slot; slots are cs elements apart (CSC = compile-time cs when known, so the
+// shared-memory loads use immediate offsets).  CP: alpha == 0, exact copy of the B-source bits.
+template <int KK, int PREC, bool MASSG, bool CP, int CSC>
+__device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, int cA, int cB, double*& om,
+                                         float*& of, int64_t L, const double* wr)
 {
 #define SLDG_DBL(j) ((PREC == SLDG_FP64) || (MASSG && (j) == 0))
+    const int cs = CSC ? CSC : cs_rt;
+    if (CP) {
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            if (SLDG_DBL(j)) {
+                __stcs(om, ((const double*)sp)[cB]);
+                om += L;
+                sp += cs * 8;
+            } else {
+                __stcs(of, ((const float*)sp)[cB]);
+                of += L;
+                sp += cs * 4;
+            }
+        }
+        return;
+    }
     double va[KK], vb[KK];
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
@@ -576,7 +595,6 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs, int c
         for (int l = 0; l < KK; ++l) o = fma(wr[j * KK + l], va[l], o);
 #pragma unroll
         for (int l = 0; l < KK; ++l) o = fma(wr[KK * KK + j * KK + l], vb[l], o);
-        if (cp) o = vb[j];  // alpha == 0: exact copy (R4); fp32 -> fp64 -> fp32 round trip is exact
         if (SLDG_DBL(j)) {
             __stcs(om, o);
             om += L;
@@ -588,24 +606,38 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs, int c
 #undef SLDG_DBL
 }
 
-// all gc coupled groups of a stage for one target cell.  Mixed: om = mass of the cell, of =
-// plane of slot q0 (or of slot 1 for the mass group); fp64: om = slot q0 of the cell.
-template <int KK, int PREC, bool MASSG>
-__device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, int cs, int cA, int cB, double* om,
-                                           float* of, int64_t L, int cp, const double* wr)
+// all gc coupled groups of a stage for one target cell (columns cA, cB of the stage rows).
+// Mixed: om = mass of the cell, of = plane of slot q0 (or of slot 1 for the mass group);
+// fp64: om = slot q0 of the cell.
+template <int KK, int PREC, bool MASSG, bool CP, int CSC>
+__device__ __forceinline__ void d0_consume_t(const unsigned char* sbase, int gc, int cs, int cA, int cB, double* om,
+                                             float* of, int64_t L, const double* wr)
 {
     const unsigned char* sp = sbase;
     int gi = 0;
     if (MASSG) {
-        d0_group<KK, PREC, true>(sp, cs, cA, cB, om, of, L, cp, wr);
+        d0_group<KK, PREC, true, CP, CSC>(sp, cs, cA, cB, om, of, L, wr);
         gi = 1;
     }
     // two groups per iteration: independent FMA chains for the scheduler to interleave
     for (; gi + 1 < gc; gi += 2) {
-        d0_group<KK, PREC, false>(sp, cs, cA, cB, om, of, L, cp, wr);
-        d0_group<KK, PREC, false>(sp, cs, cA, cB, om, of, L, cp, wr);
+        d0_group<KK, PREC, false, CP, CSC>(sp, cs, cA, cB, om, of, L, wr);
+        d0_group<KK, PREC, false, CP, CSC>(sp, cs, cA, cB, om, of, L, wr);
     }
-    if (gi < gc) d0_group<KK, PREC, false>(sp, cs, cA, cB, om, of, L, cp, wr);
+    if (gi < gc) d0_group<KK, PREC, false, CP, CSC>(sp, cs, cA, cB, om, of, L, wr);
+}
+
+template <int KK, int PREC, bool MASSG>
+__device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, int cs, int cA, int cB, double* om,
+                                           float* of, int64_t L, int cp, const double* wr)
+{
+    if (cp) {
+        d0_consume_t<KK, PREC, MASSG, true, 0>(sbase, gc, cs, cA, cB, om, of, L, wr);
+    } else if (cs == 256) {
+        d0_consume_t<KK, PREC, MASSG, false, 256>(sbase, gc, cs, cA, cB, om, of, L, wr);
+    } else {
+        d0_consume_t<KK, PREC, MASSG, false, 0>(sbase, gc, cs, cA, cB, om, of, L, wr);
+    }
 }
 
 template <int KK, int PREC>
