@@ -239,7 +239,7 @@ __device__ __forceinline__ void strided_consume(const unsigned char* const* sb, 
 //         inner: {lo, i_d, hi, plane, layer}   outer: {lo, 1, 1, plane, layer}
 // ============================================================================================
 template <int KK, int PREC>
-__global__ void __launch_bounds__(kTmaThreads) sweep_strided_tma(Layout lay, Sweep sw, Arrays src, Arrays dst,
+__global__ void __launch_bounds__(kTmaThreads, 1) sweep_strided_tma(Layout lay, Sweep sw, Arrays src, Arrays dst,
                                                                   int64_t lb, int64_t le, TmaPlan pl,
                                                                   const __grid_constant__ TmapSet tmaps)
 {
@@ -590,11 +590,14 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, in
     }
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
-        double o = 0.0;
+        // A- and B-parts as two independent FMA chains (k deep instead of 2k), then one add
+        double oa = 0.0, ob = 0.0;
 #pragma unroll
-        for (int l = 0; l < KK; ++l) o = fma(wr[j * KK + l], va[l], o);
-#pragma unroll
-        for (int l = 0; l < KK; ++l) o = fma(wr[KK * KK + j * KK + l], vb[l], o);
+        for (int l = 0; l < KK; ++l) {
+            oa = fma(wr[j * KK + l], va[l], oa);
+            ob = fma(wr[KK * KK + j * KK + l], vb[l], ob);
+        }
+        const double o = oa + ob;
         if (SLDG_DBL(j)) {
             __stcs(om, o);
             om += L;
@@ -641,7 +644,7 @@ __device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, i
 }
 
 template <int KK, int PREC>
-__global__ void __launch_bounds__(kTmaThreads) sweep_d0_tma(Layout lay, Sweep sw, Arrays src, Arrays dst, int64_t lb,
+__global__ void __launch_bounds__(kTmaThreads, 1) sweep_d0_tma(Layout lay, Sweep sw, Arrays src, Arrays dst, int64_t lb,
                                                              int64_t le, TmaPlan pl,
                                                              const __grid_constant__ TmapSet tmaps)
 {
