@@ -105,6 +105,7 @@ sldg_status ensure_weights(sldg_grid g, int64_t n_entries)
     cudaFree(g->w.smod);
     cudaFree(g->w.copy);
     cudaFree(g->w.ab);
+    cudaFree(g->w.rec);
     g->w = Weights{};
     int64_t cap = std::max<int64_t>(n_entries, 64);
     const int k = g->lay.k;
@@ -112,6 +113,7 @@ sldg_status ensure_weights(sldg_grid g, int64_t n_entries)
     CU(cudaMalloc(&g->w.smod, cap * sizeof(int64_t)));
     CU(cudaMalloc(&g->w.copy, cap * sizeof(int)));
     CU(cudaMalloc(&g->w.ab, cap * 2 * k * k * sizeof(double)));
+    CU(cudaMalloc(&g->w.rec, cap * (2 * k * k + 2) * sizeof(double)));
     g->w.cap = cap;
     return SLDG_OK;
 }
@@ -354,6 +356,7 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
     sw.smod = g->w.smod;
     sw.copy = g->w.copy;
     sw.ab = g->w.ab;
+    sw.rec = g->w.rec;
 
     const Arrays& src = g->buf[g->cur];
     const Arrays& dst = g->buf[1 - g->cur];
@@ -560,6 +563,7 @@ sldg_status sldg_destroy(sldg_grid g)
     cudaFree(g->w.smod);
     cudaFree(g->w.copy);
     cudaFree(g->w.ab);
+    cudaFree(g->w.rec);
     cudaFree(g->d_field);
     cudaFree(g->d_partials);
     cudaFree(g->d_scalar);

@@ -36,6 +36,7 @@ struct Weights {
     int64_t* smod = nullptr;   // i* mod n_d in [0, n_d) per entry
     int* copy = nullptr;       // 1 if alpha == 0 (exact rotation)
     double* ab = nullptr;      // [entry][2][k][k]: A then B, row-major
+    double* rec = nullptr;     // [entry][2k^2 + 2]: A, B, i* mod n (int64 bits), copy (int64 bits)
     int64_t cap = 0;
 };
 
@@ -64,6 +65,7 @@ struct Sweep {
     const int64_t* smod;   // i* mod nd
     const int* copy;
     const double* ab;
+    const double* rec;     // packed line records (see Weights::rec)
 };
 
 struct Grid {

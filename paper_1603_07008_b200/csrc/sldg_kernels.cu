@@ -71,10 +71,12 @@ __device__ void dev_gauss(int n, double* x, double* w)
     if (n & 1) x[n / 2] = 0.0;
 }
 
+__device__ void build_ab(int k, double a, double* A, double* B);
+
 __global__ void build_weights_kernel(int k, int64_t nd, const double* __restrict__ field, double shift,
                                      int64_t n_entries, int64_t* __restrict__ sh_raw,
                                      int64_t* __restrict__ sh_mod, int* __restrict__ cpy,
-                                     double* __restrict__ ab, int* __restrict__ err)
+                                     double* __restrict__ ab, double* __restrict__ rec, int* __restrict__ err)
 {
     int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_entries) return;
@@ -102,8 +104,16 @@ __global__ void build_weights_kernel(int k, int64_t nd, const double* __restrict
         A[j] = 0.0;
         B[j] = ((j / k) == (j % k)) ? 1.0 : 0.0;
     }
-    if (a == 0.0) return;
+    if (a != 0.0) build_ab(k, a, A, B);
+    // packed line record {A, B, i* mod n, copy} (16(k^2+1) bytes) for bulk copies into smem
+    double* r = rec + e * (2 * k * k + 2);
+    for (int j = 0; j < 2 * k * k; ++j) r[j] = A[j];
+    r[2 * k * k] = __longlong_as_double((long long)sh_mod[e]);
+    r[2 * k * k + 1] = __longlong_as_double((long long)cpy[e]);
+}
 
+__device__ void build_ab(int k, double a, double* A, double* B)
+{
     double xg[kMaxK], wg[kMaxK], Pj[kMaxK + 2], Pl[kMaxK + 2];
     dev_gauss(k, xg, wg);
     for (int j = 0; j < k * k; ++j) {
@@ -156,7 +166,7 @@ cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field,
     int threads = 128;
     int64_t blocks = (n_entries + threads - 1) / threads;
     build_weights_kernel<<<(unsigned)blocks, threads, 0, s>>>(lay.k, nd, d_field, shift, n_entries,
-                                                              w.shift, w.smod, w.copy, w.ab, d_err);
+                                                              w.shift, w.smod, w.copy, w.ab, w.rec, d_err);
     return cudaGetLastError();
 }
 

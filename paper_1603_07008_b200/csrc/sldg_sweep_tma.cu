@@ -689,47 +689,22 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sweep_d0_tma(Layout lay, Sweep
     const int ncell = (n0 <= NT) ? 1 : n0 / NT;
     const bool has_cell = !producer && my_r < R;
 
-    // the line data (shift, copy flag, A/B) of the NEXT tile is loaded while the current one
-    // streams (software prefetch), so tile boundaries do not stall the consumers
-    int64_t pf_s = 0;
-    int pf_cp = 0;
-    double pf_w[2 * KK * KK];
-    auto prefetch = [&](int64_t tl) {
-        if (!has_cell) return;
-        const int64_t blk = tl % nblk;
-        const int64_t layer = lb + tl / nblk;
-        int64_t f = 0;
-        if (sw.fmask) {
-            int64_t idx[kMaxDim];
-            int64_t rem2 = blk * R + my_r;  // line index within the layer
-#pragma unroll
-            for (int e = 0; e < kMaxDim; ++e) idx[e] = 0;
-            for (int e = 1; e < D - 1; ++e) {
-                idx[e] = rem2 % lay.n[e];
-                rem2 /= lay.n[e];
-            }
-            if (D >= 2) idx[D - 1] = lay.first_layer + layer;
-            f = tfield_index(sw, idx, D);
-        }
-        pf_s = __ldg(&sw.smod[f]);
-        pf_cp = __ldg(&sw.copy[f]);
-#pragma unroll
-        for (int i = 0; i < 2 * KK * KK; ++i) pf_w[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
-    };
-    if ((int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x);
+    // Line data (A, B, i* mod n, copy flag) travels with the tile's first stage: the producer
+    // bulk-copies the R packed line records (Weights::rec, 16(k^2+1) bytes each) into the
+    // stage's record area, so no thread waits on a global load at a tile boundary and no
+    // registers hold a prefetch.
+    const int recw = 2 * KK * KK + 2;  // doubles per record
+    const int rec_off = pl.stage_bytes - R * recw * 8;
 
     uint32_t it = 0;
+    int64_t my_s = 0;
+    int my_cp = 0;
+    double wr[2 * KK * KK];
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t blk = tile % nblk;
         const int64_t layer = lb + tile / nblk;
         const int64_t layerp = lay.pad + layer;
         const int64_t inner_base = blk * R * (int64_t)n0;  // first cell of the tile's first line
-        const int64_t my_s = pf_s;
-        const int my_cp = pf_cp;
-        double wr[2 * KK * KK];
-#pragma unroll
-        for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = pf_w[i];
-        if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
         for (int g0 = 0; g0 < G; g0 += GC) {
             const int gc = (G - g0) < GC ? (G - g0) : GC;
             const int s = it % S;
@@ -741,7 +716,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sweep_d0_tma(Layout lay, Sweep
                 if (lane == 0) {
                     mbar_wait(&empty[s], ph ^ 1);
                     const uint32_t es = (PREC == SLDG_FP64) ? 8u : 4u;
-                    const uint32_t bytes = (uint32_t)cell_stride * (BP * es + (massg ? 8u : 0u));
+                    uint32_t bytes = (uint32_t)cell_stride * (BP * es + (massg ? 8u : 0u));
+                    if (g0 == 0) bytes += (uint32_t)(R * recw * 8);
                     mbar_expect_tx(&full[s], bytes);
                     const int c1 = (int)(inner_base / box0);
                     if (massg) {
@@ -751,10 +727,37 @@ __global__ void __launch_bounds__(kTmaThreads, 1) sweep_d0_tma(Layout lay, Sweep
                         const int plane0 = (PREC == SLDG_FP64) ? g0 * KK : g0 * KK - 1;
                         tma_5d(st, &tmaps.f[0], 0, c1, 0, plane0, (int)layerp, &full[s], pol);
                     }
+                    if (g0 == 0) {
+                        for (int r = 0; r < R; ++r) {  // the tile's line records
+                            int64_t f = 0;
+                            if (sw.fmask) {  // 32-bit index math: this thread feeds the whole CTA
+                                int64_t idx[kMaxDim];
+                                uint32_t rem2 = (uint32_t)(blk * R + r);  // line index within the layer
+#pragma unroll
+                                for (int e = 0; e < kMaxDim; ++e) idx[e] = 0;
+                                for (int e = 1; e < D - 1; ++e) {
+                                    const uint32_t ne = (uint32_t)lay.n[e];
+                                    const uint32_t q = rem2 / ne;
+                                    idx[e] = rem2 - q * ne;
+                                    rem2 = q;
+                                }
+                                if (D >= 2) idx[D - 1] = lay.first_layer + layer;
+                                f = tfield_index(sw, idx, D);
+                            }
+                            bulk_g2s(st + rec_off + r * recw * 8, sw.rec + f * recw, (uint32_t)(recw * 8), &full[s], pol);
+                        }
+                    }
                 }
                 __syncwarp();
             } else {
                 mbar_wait(&full[s], ph);
+                if (g0 == 0 && has_cell) {  // this tile's line data for my line
+                    const double* rp = (const double*)(st + rec_off) + my_r * recw;
+#pragma unroll
+                    for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = rp[i];
+                    my_s = __double_as_longlong(rp[2 * KK * KK]);
+                    my_cp = (int)__double_as_longlong(rp[2 * KK * KK + 1]);
+                }
                 if (has_cell) {
                     for (int ci = 0; ci < ncell; ++ci) {
                         const int cc = my_c0 + ci * NT;  // column (target cell within the line)
@@ -883,7 +886,10 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
         if (cs % pl->W != 0 || cs / pl->W > 256 || lay.L % pl->W != 0) return false;
         const int es = (lay.prec == SLDG_FP64) ? 8 : 4;
         // stage: [mass (mixed mass group)] + GC*k planes (the mass group's box holds one spare plane)
-        pl->stage_bytes = (int)((cs * (GC * k * es + ((lay.prec == SLDG_FP64) ? 0 : 8)) + 127) / 128 * 128);
+        // + the tile's R packed line records at the end (16-byte aligned: 16(k^2+1) bytes each)
+        // (stage starts stay 128-byte aligned for the tensor copies; records end the stage)
+        pl->stage_bytes = (int)(((cs * (GC * k * es + ((lay.prec == SLDG_FP64) ? 0 : 8)) + 127) / 128 * 128 +
+                                 R * (2 * k * k + 2) * 8 + 127) / 128 * 128);
         pl->stages = (int)std::min<int64_t>(8, budget / pl->stage_bytes);
         return pl->stages >= 2;
     }
