@@ -134,6 +134,7 @@ struct TmaPlan {
     int GC = 0;     // d0: coupled groups per stage
     int stage_bytes = 0;
     int stages = 0;
+    int ctas = 1;   // CTAs per SM (shared-memory budget and register bound of the instance)
 };
 bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl);
 const char* sweep_kernel_name(const Layout& lay, const Sweep& sw);

@@ -238,8 +238,8 @@ __device__ __forceinline__ void strided_consume(const unsigned char* const* sb, 
 //   tensor maps (5D, fp32 planes or fp64 slots / fp64 mass):
 //         inner: {lo, i_d, hi, plane, layer}   outer: {lo, 1, 1, plane, layer}
 // ============================================================================================
-template <int KK, int PREC>
-__global__ void __launch_bounds__(kTmaThreads, 1) sweep_strided_tma(Layout lay, Sweep sw, Arrays src, Arrays dst,
+template <int KK, int PREC, int MINB>
+__global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout lay, Sweep sw, Arrays src, Arrays dst,
                                                                   int64_t lb, int64_t le, TmaPlan pl,
                                                                   const __grid_constant__ TmapSet tmaps)
 {
@@ -643,8 +643,8 @@ __device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, i
     }
 }
 
-template <int KK, int PREC>
-__global__ void __launch_bounds__(kTmaThreads, 1) sweep_d0_tma(Layout lay, Sweep sw, Arrays src, Arrays dst, int64_t lb,
+template <int KK, int PREC, int MINB>
+__global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sweep sw, Arrays src, Arrays dst, int64_t lb,
                                                              int64_t le, TmaPlan pl,
                                                              const __grid_constant__ TmapSet tmaps)
 {
@@ -850,10 +850,17 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
     if (!encoder()) return false;
     const int64_t n0 = lay.n[0];
     const int k = lay.k;
-    const int64_t budget = std::min<int64_t>(g_smem_optin, 200 * 1024) - 256;
+    // CTAs per SM (SLDG_TMA_CTAS=2: two CTAs, each with half the shared memory and <= 96
+    // registers per thread -- twice the warps to hide latency, at the cost of spills)
+    // Measured: k <= 2 fits 96 registers without hurtful spills and gains from the extra warps
+    // (C4 64^4 k=2: 375 -> 467 GDoF/s); k = 3 loses (C5: 693 -> 643 GDoF/s).
+    int ctas = (k <= 2) ? 2 : 1;
+    if (const char* e = getenv("SLDG_TMA_CTAS")) ctas = (atoi(e) == 2) ? 2 : 1;
+    const int64_t budget = std::min<int64_t>(g_smem_optin, 200 * 1024) / ctas - 256 - (ctas - 1) * 1024;
     const int bpc_max = (lay.prec == SLDG_FP64) ? 8 * k : 8 + 4 * (k - 1);  // bytes per column, mass group
     const int NT = kTmaConsumerWarps * 32;
     *pl = TmaPlan{};
+    pl->ctas = ctas;
     if (k > 4) return false;  // line weights live in registers; larger k uses the register kernels
     if (n0 % 4 != 0) return false;
     const int64_t layers_alloc = lay.layers + 2 * lay.pad;
@@ -1044,14 +1051,14 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
     if (!cached_tmaps(lay, sw, src, pl, &tmaps)) return cudaErrorInvalidValue;
     const size_t smem = 256 + (size_t)pl.stages * pl.stage_bytes;
     int64_t ntiles;
-    const int per_sm = std::max<int>(1, (int)(228 * 1024 / (smem + 1024)));
+    const int per_sm = pl.ctas;  // CTAs per SM the plan sized shared memory for
     if (sw.dim == 0) {
         ntiles = (lay.L / lay.n[0] / pl.R) * (le - lb);
-        auto kern = sweep_d0_tma<KK, PREC>;
-        static bool attr_set = false;  // once per instantiation: allow the full opt-in carveout
-        if (!attr_set) {
+        auto kern = (pl.ctas == 2) ? sweep_d0_tma<KK, PREC, 2> : sweep_d0_tma<KK, PREC, 1>;
+        static bool attr_set[3] = {false, false, false};  // once per instantiation: full opt-in carveout
+        if (!attr_set[pl.ctas]) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
-            attr_set = true;
+            attr_set[pl.ctas] = true;
         }
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
@@ -1064,11 +1071,11 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         if (!outer)
             for (int e = sw.dim + 1; e < lay.D - 1; ++e) M_hi *= lay.n[e];
         ntiles = ((nline + pl.T - 1) / pl.T) * (M_lo / pl.W) * M_hi * (outer ? 1 : (le - lb));
-        auto kern = sweep_strided_tma<KK, PREC>;
-        static bool attr_set = false;  // once per instantiation: allow the full opt-in carveout
-        if (!attr_set) {
+        auto kern = (pl.ctas == 2) ? sweep_strided_tma<KK, PREC, 2> : sweep_strided_tma<KK, PREC, 1>;
+        static bool attr_set[3] = {false, false, false};  // once per instantiation: full opt-in carveout
+        if (!attr_set[pl.ctas]) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
-            attr_set = true;
+            attr_set[pl.ctas] = true;
         }
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
