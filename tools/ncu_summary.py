@@ -62,11 +62,12 @@ def launches(path, out, dram_json=None, key=None):
     if dram_json and key:
         db = json.load(open(dram_json)) if os.path.exists(dram_json) else {}
         sweeps = [d for d in per.values() if "sweep" in d["name"]]
-        # sweeps are launched in dim order within each split step
+        # sweeps are launched in dim order within each split step; take the first timed step
+        # (after bench.py's default 3 warm-up steps), not the e2e / precision-comparison runs
         ndim = int(key.split("_D")[-1]) if "_D" in key else 4
         base = key.split("_D")[0]
-        last = sweeps[-ndim:]
-        for dim, d in enumerate(last):
+        first = sweeps[3 * ndim:4 * ndim]
+        for dim, d in enumerate(first):
             db[f"{base}_dim{dim}"] = d.get("read", 0) + d.get("write", 0)
         json.dump(db, open(dram_json, "w"), indent=1, sort_keys=True)
     print(out)
