@@ -101,6 +101,13 @@ typedef struct {
  * < world), ENOMEM, ECUDA, ENCCL. */
 sldg_status sldg_create(const sldg_grid_desc* grid, int k, const sldg_domain* dom,
                         sldg_precision prec, const sldg_dist* dist, sldg_grid* out);
+/* General precision layout (the paper's "# double", SS III-A, Tables II-VI): coefficient slots
+ * q < n_double (linear index of the host layout) are stored in fp64, the others in fp32
+ * (RNE); arithmetic is fp64 either way.  n_double = 1 is SLDG_MIXED, n_double = k^D is
+ * SLDG_FP64, n_double = 0 is pure fp32 storage (mass no longer conserved to fp64).
+ * Values other than 1 and k^D: 1D grids only (ENOTSUP otherwise). */
+sldg_status sldg_create_ex(const sldg_grid_desc* grid, int k, const sldg_domain* dom, int n_double,
+                           const sldg_dist* dist, sldg_grid* out);
 sldg_status sldg_destroy(sldg_grid g);
 
 /* Copy n_cells cells starting at local cell first_cell from host fp64 (layout above) into

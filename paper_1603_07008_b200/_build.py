@@ -1,7 +1,8 @@
 """Build the in-tree shared library libsldg.so for sm_100a with nvcc (no JIT, no torch ext).
 
-nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo, linked against the NCCL that
-ships with torch (same soname as the one torch loads, so one NCCL per process).
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo, one object per .cu compiled in
+parallel, linked against the NCCL that ships with torch (same soname as the one torch loads, so
+one NCCL per process) and the static CUDA runtime.
 """
 from __future__ import annotations
 
@@ -9,6 +10,7 @@ import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -34,24 +36,38 @@ def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
+def headers():
+    return glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
+
+
 def needs_build() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = sources() + glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(ROOT, "include", "*.h"))
-    return any(os.path.getmtime(p) > t for p in deps)
+    return any(os.path.getmtime(p) > t for p in sources() + headers())
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not needs_build():
         return LIB
     inc, lib = nccl_paths()
-    cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared", "-Xcompiler", "-fPIC",
-           "-Xptxas", "-v" if verbose else "-O3",
-           f"-I{inc}", f"-I{os.path.join(ROOT, 'include')}",
-           "-o", LIB + ".tmp", *sources(),
-           f"-L{lib}", "-l:libnccl.so.2", "-Xlinker", f"-rpath={lib}", "-cudart", "static"]
-    subprocess.check_call(cmd)
+    objdir = os.path.join(HERE, "build_obj")
+    os.makedirs(objdir, exist_ok=True)
+    hdr_t = max(os.path.getmtime(p) for p in headers())
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{inc}",
+             f"-I{os.path.join(ROOT, 'include')}"] + (["-Xptxas", "-v"] if verbose else [])
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(os.path.getmtime(src), hdr_t):
+            subprocess.check_call([NVCC, *flags, "-c", "-o", obj + ".tmp", src])
+            os.replace(obj + ".tmp", obj)
+        return obj
+
+    with ThreadPoolExecutor(max_workers=len(sources())) as ex:
+        objs = list(ex.map(compile_one, sources()))
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", LIB + ".tmp", *objs, f"-L{lib}", "-l:libnccl.so.2",
+                           "-Xlinker", f"-rpath={lib}", "-cudart", "static"])
     os.replace(LIB + ".tmp", LIB)
     return LIB
 

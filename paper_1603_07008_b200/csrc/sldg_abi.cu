@@ -72,30 +72,25 @@ int owner_of(int64_t n, int world, int64_t layer, int64_t* local)
     return -1;
 }
 
-size_t bytes_per_cell(const Layout& L)
-{
-    return L.prec == SLDG_FP64 ? (size_t)8 * L.K : (size_t)8 + (size_t)4 * (L.K - 1);
-}
+// 8 nd + 4 (K - nd) bytes per stored cell (S:163-169 generalised; the paper's (o, d))
+size_t bytes_per_cell(const Layout& L) { return (size_t)8 * L.nd + (size_t)4 * (L.K - L.nd); }
 
+// One array: nd fp64 planes per layer, then (K - nd) fp32 planes per layer (sldg_internal.h)
 Arrays arrays_of(const Layout& L, void* base)
 {
     Arrays a;
     const size_t rows = (size_t)(L.layers + 2 * L.pad) * (size_t)L.L;
-    if (L.prec == SLDG_FP64) {
-        a.s64 = (double*)base;
-    } else {
-        a.mass = (double*)base;
-        size_t off = ((rows * 8 + 255) / 256) * 256;
-        a.pl = (float*)((char*)base + off);
-    }
+    a.mass = (double*)base;
+    if (L.prec == SLDG_FP64) a.s64 = a.mass;
+    size_t off = ((rows * 8 * (size_t)L.nd + 255) / 256) * 256;
+    a.pl = (L.nd < L.K) ? (float*)((char*)base + off) : nullptr;
     return a;
 }
 
 size_t array_alloc_bytes(const Layout& L)
 {
     const size_t rows = (size_t)(L.layers + 2 * L.pad) * (size_t)L.L;
-    if (L.prec == SLDG_FP64) return rows * 8 * (size_t)L.K;
-    return ((rows * 8 + 255) / 256) * 256 + rows * 4 * (size_t)(L.K - 1);
+    return ((rows * 8 * (size_t)L.nd + 255) / 256) * 256 + rows * 4 * (size_t)(L.K - L.nd);
 }
 
 sldg_status ensure_weights(sldg_grid g, int64_t n_entries)
@@ -241,18 +236,16 @@ sldg_status halo_exchange(sldg_grid g, const Arrays& a, int64_t left, int64_t ri
     const size_t mass_elems = (size_t)L.L;
     const size_t pl_elems = (size_t)L.L * (size_t)(L.K - 1);
     const size_t s64_elems = (size_t)L.L * (size_t)L.K;
+    (void)mass_elems;
+    (void)s64_elems;
+    (void)pl_elems;
+    // one layer of all slots: nd fp64 planes (one chunk) + (K - nd) fp32 planes (one chunk)
     auto layer_ptrs = [&](int64_t lp, void** p0, size_t* c0, void** p1, size_t* c1) {
-        if (L.prec == SLDG_FP64) {
-            *p0 = a.s64 + (size_t)lp * s64_elems;
-            *c0 = s64_elems;
-            *p1 = nullptr;
-            *c1 = 0;
-        } else {
-            *p0 = a.mass + (size_t)lp * mass_elems;
-            *c0 = mass_elems;
-            *p1 = a.pl + (size_t)lp * pl_elems;
-            *c1 = pl_elems;
-        }
+        const size_t dn = (size_t)L.L * (size_t)L.nd, fn = (size_t)L.L * (size_t)(L.K - L.nd);
+        *p0 = a.mass + (size_t)lp * dn;
+        *c0 = dn;
+        *p1 = fn ? (void*)(a.pl + (size_t)lp * fn) : nullptr;
+        *c1 = fn;
     };
     std::vector<Xfer> xs = halo_plan(n, g->world, g->rank, L.pad, left, right);
     for (const Xfer& x : xs) {  // layers this rank owns itself (wrap-around): device copies
@@ -439,14 +432,38 @@ sldg_status sldg_layer_owner(int64_t n, int world, int64_t layer, int* owner, in
     return SLDG_OK;
 }
 
+static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_domain* dom, int prec, int nd_req,
+                               const sldg_dist* dist, sldg_grid* out);
+
 sldg_status sldg_create(const sldg_grid_desc* grid, int k, const sldg_domain* dom, sldg_precision prec,
                         const sldg_dist* dist, sldg_grid* out)
+{
+    if (prec != SLDG_MIXED && prec != SLDG_FP64) return fail(SLDG_EINVAL, "bad precision");
+    return create_impl(grid, k, dom, prec, -1, dist, out);
+}
+
+sldg_status sldg_create_ex(const sldg_grid_desc* grid, int k, const sldg_domain* dom, int n_double,
+                           const sldg_dist* dist, sldg_grid* out)
+{
+    if (!grid || grid->ndim < 1 || grid->ndim > SLDG_MAX_DIM || k < 1 || k > SLDG_MAX_K)
+        return fail(SLDG_EINVAL, "bad grid or k");
+    int64_t K = 1;
+    for (int d = 0; d < grid->ndim; ++d) K *= k;
+    if (n_double < 0 || n_double > K) return fail(SLDG_EINVAL, "n_double must be in 0..k^D");
+    if (n_double == 1) return create_impl(grid, k, dom, SLDG_MIXED, 1, dist, out);
+    if (n_double == K) return create_impl(grid, k, dom, SLDG_FP64, (int)K, dist, out);
+    if (grid->ndim != 1)
+        return fail(SLDG_ENOTSUP, "n_double other than 1 or k^D is supported for 1D grids (the paper's tables)");
+    return create_impl(grid, k, dom, SLDG_GENERAL, n_double, dist, out);
+}
+
+static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_domain* dom, int prec, int nd_req,
+                               const sldg_dist* dist, sldg_grid* out)
 {
     if (!grid || !dom || !out) return fail(SLDG_EINVAL, "null argument");
     *out = nullptr;
     if (grid->ndim < 1 || grid->ndim > SLDG_MAX_DIM) return fail(SLDG_EINVAL, "ndim must be in 1..6");
     if (k < 1 || k > SLDG_MAX_K) return fail(SLDG_EINVAL, "k must be in 1..8");
-    if (prec != SLDG_MIXED && prec != SLDG_FP64) return fail(SLDG_EINVAL, "bad precision");
     const int D = grid->ndim;
     int64_t K = 1;
     for (int d = 0; d < D; ++d) {
@@ -474,6 +491,7 @@ sldg_status sldg_create(const sldg_grid_desc* grid, int k, const sldg_domain* do
     L.k = k;
     L.K = (int)K;
     L.prec = prec;
+    L.nd = (prec == SLDG_MIXED) ? 1 : (prec == SLDG_FP64) ? (int)K : nd_req;
     int64_t S = 1;
     for (int d = 0; d < kMaxDim; ++d) {
         L.n[d] = d < D ? grid->cells[d] : 1;
@@ -594,7 +612,7 @@ sldg_status sldg_set_coeffs(sldg_grid g, const double* src, int64_t first_cell, 
     for (int64_t e = 0; e < n; ++e) {  // all-or-nothing validation
         double v = src[e];
         if (!isfinite(v)) return fail(SLDG_EINVAL, "non-finite coefficient at element " + std::to_string(e));
-        if (L.prec == SLDG_MIXED && (e % L.K) != 0 && fabs(v) > (double)FLT_MAX)
+        if ((e % L.K) >= L.nd && fabs(v) > (double)FLT_MAX)
             return fail(SLDG_EINVAL, "value beyond FLT_MAX in an fp32 slot at element " + std::to_string(e));
     }
     sldg_status st = ensure_stage(g);

@@ -23,12 +23,28 @@ namespace sldg {
 constexpr int kMaxDim = SLDG_MAX_DIM;
 constexpr int kMaxK = SLDG_MAX_K;
 
-// One coefficient array (a ping-pong buffer).
+// One coefficient array (a ping-pong buffer).  General addressing (any nd):
+//   slot q <  nd: mass[((pad + layer) * nd + q) * L + inner]            (fp64)
+//   slot q >= nd: pl  [((pad + layer) * (K - nd) + (q - nd)) * L + inner] (fp32)
+// which is the mixed layout for nd = 1 and the fp64 layout (s64 == mass) for nd = K.
 struct Arrays {
-    double* mass = nullptr;  // mixed: fp64 slot 0
-    float* pl = nullptr;     // mixed: fp32 slots 1..K-1
+    double* mass = nullptr;  // fp64 slots (mixed: slot 0; fp64 variant: all, == s64)
+    float* pl = nullptr;     // fp32 slots
     double* s64 = nullptr;   // fp64 variant: all slots
 };
+
+constexpr int SLDG_GENERAL = 2;  // internal precision tag: 1D grid with an arbitrary nd
+
+__host__ __device__ __forceinline__ double* dslot(const Arrays& a, int64_t layerp, int nd, int q, int64_t L,
+                                                  int64_t inner)
+{
+    return a.mass + (layerp * nd + q) * L + inner;
+}
+__host__ __device__ __forceinline__ float* fslot(const Arrays& a, int64_t layerp, int K, int nd, int q, int64_t L,
+                                                 int64_t inner)
+{
+    return a.pl + (layerp * (K - nd) + (q - nd)) * L + inner;
+}
 
 // Per-sweep weight table: one entry per field entry (or a single one for a constant shift).
 struct Weights {
@@ -45,7 +61,8 @@ struct Layout {
     int D;
     int k;
     int K;            // k^D
-    int prec;         // SLDG_MIXED / SLDG_FP64
+    int prec;         // SLDG_MIXED (nd = 1) / SLDG_FP64 (nd = K) / SLDG_GENERAL (1D, any nd)
+    int nd;           // number of leading slots q < nd stored in fp64 (the paper's "# double")
     int64_t n[kMaxDim];   // GLOBAL extents
     int64_t S[kMaxDim];   // inner strides S_d (d < D-1); S_{D-1} unused
     int64_t L;            // cells per layer
@@ -138,6 +155,10 @@ struct TmaPlan {
 };
 bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl);
 const char* sweep_kernel_name(const Layout& lay, const Sweep& sw);
+// 1D sweeps, any precision layout (sldg_line.cu)
+cudaError_t launch_line(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst, cudaStream_t s,
+                        const char** name);
+const char* line_kernel_name(const Layout& lay);
 cudaError_t launch_sweep_tma(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
                              int64_t layer_begin, int64_t layer_end, const TmaPlan& pl, cudaStream_t s);
 

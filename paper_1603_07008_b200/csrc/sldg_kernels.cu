@@ -15,6 +15,18 @@
 
 namespace sldg {
 
+// slot q of a cell at (padded layer lp, inner) through the general nd layout (sldg_internal.h)
+__device__ __forceinline__ double load_slot(const Layout& L, const Arrays& a, int q, int64_t lp, int64_t inner)
+{
+    if (q < L.nd) return *dslot(a, lp, L.nd, q, L.L, inner);
+    return (double)*fslot(a, lp, L.K, L.nd, q, L.L, inner);
+}
+__device__ __forceinline__ void store_slot(const Layout& L, const Arrays& a, int q, int64_t lp, int64_t inner, double v)
+{
+    if (q < L.nd) *dslot(a, lp, L.nd, q, L.L, inner) = v;
+    else *fslot(a, lp, L.K, L.nd, q, L.L, inner) = __double2float_rn(v);
+}
+
 // ============================================================================================
 // a1 + a2: shift decomposition and weight build, one thread per field entry.
 // A_jl = (2j+1)/2 int_{-1}^{2a-1} P_l(xi+2-2a) P_j(xi) dxi,  B_jl = (2j+1)/2 int_{2a-1}^{1}
@@ -189,9 +201,7 @@ __global__ void __launch_bounds__(256) mass_partials_kernel(Layout lay, Arrays a
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < lay.cells; e += stride) {
         int64_t layer = e / lay.L, inner = e - layer * lay.L;
-        double x = (lay.prec == SLDG_FP64) ? a.s64[((lay.pad + layer) * lay.K) * lay.L + inner]
-                                           : a.mass[(lay.pad + layer) * lay.L + inner];
-        neumaier_add(s, c, x);
+        neumaier_add(s, c, load_slot(lay, a, 0, lay.pad + layer, inner));
     }
     sh[threadIdx.x] = s + c;
     __syncthreads();
@@ -234,11 +244,7 @@ __global__ void set_kernel(Layout lay, Arrays a, const double* __restrict__ srcv
     int64_t cell = first_cell + e / lay.K;
     int q = (int)(e % lay.K);
     int64_t layer = cell / lay.L, inner = cell - layer * lay.L;
-    double v = srcv[e];
-    int64_t lp = lay.pad + layer;
-    if (lay.prec == SLDG_FP64) a.s64[(lp * lay.K + q) * lay.L + inner] = v;
-    else if (q == 0) a.mass[lp * lay.L + inner] = v;
-    else a.pl[(lp * (lay.K - 1) + (q - 1)) * lay.L + inner] = __double2float_rn(v);
+    store_slot(lay, a, q, lay.pad + layer, inner, srcv[e]);
 }
 
 __global__ void get_kernel(Layout lay, Arrays a, double* __restrict__ dstv, int64_t first_cell, int64_t n_elems)
@@ -248,12 +254,7 @@ __global__ void get_kernel(Layout lay, Arrays a, double* __restrict__ dstv, int6
     int64_t cell = first_cell + e / lay.K;
     int q = (int)(e % lay.K);
     int64_t layer = cell / lay.L, inner = cell - layer * lay.L;
-    int64_t lp = lay.pad + layer;
-    double v;
-    if (lay.prec == SLDG_FP64) v = a.s64[(lp * lay.K + q) * lay.L + inner];
-    else if (q == 0) v = a.mass[lp * lay.L + inner];
-    else v = (double)a.pl[(lp * (lay.K - 1) + (q - 1)) * lay.L + inner];
-    dstv[e] = v;
+    dstv[e] = load_slot(lay, a, q, lay.pad + layer, inner);
 }
 
 cudaError_t launch_set(const Layout& lay, const Arrays& a, const double* d_src, int64_t first_cell,
@@ -322,10 +323,7 @@ __global__ void fill_random_kernel(Layout lay, Arrays a, uint64_t seed)
         v = __ddiv_rn(r, wide ? pd : __ull2double_rn(p));
     }
     int64_t layer = cell / lay.L, inner = cell - layer * lay.L;
-    int64_t lp = lay.pad + layer;
-    if (lay.prec == SLDG_FP64) a.s64[(lp * lay.K + q) * lay.L + inner] = v;
-    else if (q == 0) a.mass[lp * lay.L + inner] = v;
-    else a.pl[(lp * (lay.K - 1) + (q - 1)) * lay.L + inner] = __double2float_rn(v);
+    store_slot(lay, a, q, lay.pad + layer, inner, v);
 }
 
 cudaError_t launch_fill_random(const Layout& lay, const Arrays& a, uint64_t seed, cudaStream_t s)
@@ -365,10 +363,7 @@ __global__ void fill_separable_kernel(Layout lay, Arrays a, int n_terms, const d
         for (int d = 0; d < lay.D; ++d) p *= tab[t * term_stride + off[d] + idx[d] * lay.k + m[d]];
         v += p;
     }
-    int64_t lp = lay.pad + layer;
-    if (lay.prec == SLDG_FP64) a.s64[(lp * lay.K + q) * lay.L + inner] = v;
-    else if (q == 0) a.mass[lp * lay.L + inner] = v;
-    else a.pl[(lp * (lay.K - 1) + (q - 1)) * lay.L + inner] = __double2float_rn(v);
+    store_slot(lay, a, q, lay.pad + layer, inner, v);
 }
 
 cudaError_t launch_fill_separable(const Layout& lay, const Arrays& a, int n_terms, const double* d_tables,

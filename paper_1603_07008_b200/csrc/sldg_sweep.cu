@@ -423,6 +423,7 @@ static cudaError_t launch_sweep_p(const Layout& lay, const Sweep& sw, const Arra
 const char* sweep_kernel_name(const Layout& lay, const Sweep& sw)
 {
     const char* e = getenv("SLDG_SWEEP");
+    if (lay.D == 1 && (!(e && e[0] == 'r') || lay.prec == SLDG_GENERAL)) return line_kernel_name(lay);
     TmaPlan pl;
     const bool tma = !(e && e[0] == 'r') && tma_plan(lay, sw, &pl);
     if (sw.dim == 0) return tma ? "sweep_d0_tma" : "sweep_d0_kernel";
@@ -440,6 +441,8 @@ cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, 
         const char* e = getenv("SLDG_SWEEP");
         mode = (e && e[0] == 'r') ? 0 : 1;
     }
+    // 1D grids (the paper's workload, any precision layout): the line kernels (sldg_line.cu)
+    if (lay.D == 1 && (mode == 1 || lay.prec == SLDG_GENERAL)) return launch_line(lay, sw, src, dst, s, nullptr);
     TmaPlan pl;
     if (mode == 1 && tma_plan(lay, sw, &pl)) return launch_sweep_tma(lay, sw, src, dst, layer_begin, layer_end, pl, s);
     if (lay.prec == SLDG_FP64) return launch_sweep_p<SLDG_FP64>(lay, sw, src, dst, layer_begin, layer_end, s);

@@ -21,7 +21,7 @@ STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "E
 
 # every symbol include/sldg.h declares
 EXPORTS = [
-    "sldg_create", "sldg_destroy", "sldg_set_coeffs", "sldg_get_coeffs", "sldg_advect",
+    "sldg_create", "sldg_create_ex", "sldg_destroy", "sldg_set_coeffs", "sldg_get_coeffs", "sldg_advect",
     "sldg_advect_device", "sldg_mass", "sldg_shard_info", "sldg_sync", "sldg_set_stream",
     "sldg_get_stream", "sldg_memory_bytes", "sldg_last_error", "sldg_fill_random",
     "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
@@ -67,6 +67,8 @@ def lib():
     sig = {
         "sldg_create": [ctypes.POINTER(GridDesc), ctypes.c_int, ctypes.POINTER(Domain), ctypes.c_int,
                         ctypes.POINTER(Dist), ctypes.POINTER(vp)],
+        "sldg_create_ex": [ctypes.POINTER(GridDesc), ctypes.c_int, ctypes.POINTER(Domain), ctypes.c_int,
+                           ctypes.POINTER(Dist), ctypes.POINTER(vp)],
         "sldg_destroy": [vp],
         "sldg_set_coeffs": [vp, dp, i64, i64],
         "sldg_get_coeffs": [vp, dp, i64, i64],
@@ -155,7 +157,12 @@ class Grid:
         gd = GridDesc(self.D, (ctypes.c_int64 * MAX_DIM)(*(cells + [1] * (MAX_DIM - self.D))))
         dom = Domain((ctypes.c_double * MAX_DIM)(*(lo + [0.0] * (MAX_DIM - self.D))),
                      (ctypes.c_double * MAX_DIM)(*(hi + [1.0] * (MAX_DIM - self.D))))
-        prec = {"mixed": SLDG_MIXED, "fp64": SLDG_FP64}[precision]
+        n_double = None
+        if isinstance(precision, int):  # the paper's "# double": number of leading fp64 slots
+            n_double = precision
+            prec = SLDG_MIXED
+        else:
+            prec = {"mixed": SLDG_MIXED, "fp64": SLDG_FP64}[precision]
         dist_p = None
         self._uid = None
         if world > 1 or force_halo:
@@ -166,7 +173,11 @@ class Grid:
             self._dist = Dist(rank, world, uid, None, max_halo, SLDG_DIST_FORCE_HALO if force_halo else 0)
             dist_p = ctypes.byref(self._dist)
         h = ctypes.c_void_p()
-        _check(lib().sldg_create(ctypes.byref(gd), self.k, ctypes.byref(dom), prec, dist_p, ctypes.byref(h)))
+        if n_double is None:
+            _check(lib().sldg_create(ctypes.byref(gd), self.k, ctypes.byref(dom), prec, dist_p, ctypes.byref(h)))
+        else:  # general layout: slots q < n_double in fp64 (sldg_create_ex)
+            _check(lib().sldg_create_ex(ctypes.byref(gd), self.k, ctypes.byref(dom), int(n_double), dist_p,
+                                        ctypes.byref(h)))
         self.h = h
         fl, nl = ctypes.c_int64(), ctypes.c_int64()
         _check(lib().sldg_shard_info(self.h, ctypes.byref(fl), ctypes.byref(nl)))
