@@ -96,6 +96,7 @@ size_t array_alloc_bytes(const Layout& L)
 sldg_status ensure_weights(sldg_grid g, int64_t n_entries)
 {
     if (g->w.cap >= n_entries) return SLDG_OK;
+    g->w_const = false;
     cudaFree(g->w.shift);
     cudaFree(g->w.smod);
     cudaFree(g->w.copy);
@@ -343,8 +344,13 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
         imax = r[1];
         if (imin > imax) imin = imax = 0;  // all entries invalid: lines are copied (error sticky)
     }
-    CU(launch_weights(L, sw.nd, dfield, shift, n_entries, g->w, g->d_err, g->stream));
-    g->launches += 1;
+    if (field || !g->w_const || g->w_shift != shift || g->w_n != sw.nd) {
+        CU(launch_weights(L, sw.nd, dfield, shift, n_entries, g->w, g->d_err, g->stream));
+        g->launches += 1;
+        g->w_const = !field;
+        g->w_shift = shift;
+        g->w_n = sw.nd;
+    }
     sw.shift = g->w.shift;
     sw.smod = g->w.smod;
     sw.copy = g->w.copy;

@@ -94,6 +94,11 @@ struct Grid {
     void* alloc[2] = {nullptr, nullptr};
     size_t alloc_bytes = 0;
     Weights w;
+    // the weight table holds the constant shift w_shift along an extent of w_n (no field):
+    // a repeated constant-shift sweep reuses it instead of relaunching the build kernel
+    bool w_const = false;
+    double w_shift = 0.0;
+    int64_t w_n = 0;
     double* d_field = nullptr;
     int64_t field_cap = 0;
     double* d_partials = nullptr;  // mass partial sums

@@ -109,6 +109,89 @@ __global__ void __launch_bounds__(256) line_simple_kernel(Layout lay, Sweep sw, 
 }
 
 // ============================================================================================
+// Consumer side of line_tma_kernel for one stage.  A thread owns 4 consecutive targets
+// i0..i0+3 of the tile: their sources are the 5 consecutive window cells i0..i0+4 (target r reads
+// A from cell r and B from cell r+1), so every source is read from shared memory and promoted
+// once, and the 4 outputs of a slot leave as one 16-byte (fp32) or two 16-byte (fp64) stores.
+// OFF = (w0 mod 4) is the window's offset inside its 16-byte-aligned copy; it is the same for
+// every tile of a launch (t0 is a multiple of 256), so it is a template parameter and all
+// register indexing below is static.
+template <int KK, int NDJ, int OFF>
+__device__ __forceinline__ void line_consume_stage(const unsigned char* st, int slot_elems, int nt, int64_t N,
+                                                   int64_t t0, const double (&wr)[2 * KK * KK], int cp,
+                                                   const Arrays& dst)
+{
+    constexpr int NT = kTmaConsumerWarps * 32;
+    for (int u = threadIdx.x; 4 * u < nt; u += NT) {
+        double v[KK][5];
+        if (cp) {  // alpha == 0: target r is source r+1, copied bit for bit (R4)
+            int soff = 0;
+#pragma unroll
+            for (int j = 0; j < KK; ++j) {
+                if (j < NDJ) {
+                    const double2* p = (const double2*)(st + soff) + 2 * u;
+                    const double2 a = p[0], b = p[1], c = p[2];
+                    const double e[6] = {a.x, a.y, b.x, b.y, c.x, c.y};
+                    double2* q = (double2*)dslot(dst, 0, NDJ, j, N, t0 + 4 * u);
+                    __stcs(q, make_double2(e[(OFF & 1) + 1], e[(OFF & 1) + 2]));
+                    __stcs(q + 1, make_double2(e[(OFF & 1) + 3], e[(OFF & 1) + 4]));
+                    soff += slot_elems * 8;
+                } else {
+                    const float4* p = (const float4*)(st + soff) + u;
+                    const float4 a = p[0], b = p[1];
+                    const float e[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+                    __stcs((float4*)fslot(dst, 0, KK, NDJ, j, N, t0 + 4 * u),
+                           make_float4(e[OFF + 1], e[OFF + 2], e[OFF + 3], e[OFF + 4]));
+                    soff += slot_elems * 4;
+                }
+            }
+            continue;
+        }
+        int soff = 0;
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            if (j < NDJ) {
+                const double2* p = (const double2*)(st + soff) + 2 * u;
+                const double2 a = p[0], b = p[1], c = p[2];
+                const double e[6] = {a.x, a.y, b.x, b.y, c.x, c.y};
+#pragma unroll
+                for (int r = 0; r < 5; ++r) v[j][r] = e[(OFF & 1) + r];
+                soff += slot_elems * 8;
+            } else {
+                const float4* p = (const float4*)(st + soff) + u;
+                const float4 a = p[0], b = p[1];
+                const float e[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+                for (int r = 0; r < 5; ++r) v[j][r] = (double)e[OFF + r];
+                soff += slot_elems * 4;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            double o[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                double oa = 0.0, ob = 0.0;
+#pragma unroll
+                for (int l = 0; l < KK; ++l) {
+                    oa = fma(wr[j * KK + l], v[l][r], oa);
+                    ob = fma(wr[KK * KK + j * KK + l], v[l][r + 1], ob);
+                }
+                o[r] = oa + ob;
+            }
+            if (j < NDJ) {
+                double2* q = (double2*)dslot(dst, 0, NDJ, j, N, t0 + 4 * u);
+                __stcs(q, make_double2(o[0], o[1]));
+                __stcs(q + 1, make_double2(o[2], o[3]));
+            } else {
+                __stcs((float4*)fslot(dst, 0, KK, NDJ, j, N, t0 + 4 * u),
+                       make_float4(__double2float_rn(o[0]), __double2float_rn(o[1]), __double2float_rn(o[2]),
+                                   __double2float_rn(o[3])));
+            }
+        }
+    }
+}
+
 template <int KK, int NDJ>
 __global__ void __launch_bounds__(kTmaThreads, 1) line_tma_kernel(Layout lay, Sweep sw, Arrays src, Arrays dst,
                                                                    LinePlan lp)
@@ -138,8 +221,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1) line_tma_kernel(Layout lay, Sw
     double wr[2 * KK * KK];
 #pragma unroll
     for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[i]);
-    const int NT = NC * 32;
-
     uint32_t it = 0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++it) {
         const int64_t t0 = tile * Wt;
@@ -180,38 +261,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1) line_tma_kernel(Layout lay, Sw
             __syncwarp();
         } else {
             l_wait(&full[st_i], ph);
-            // window start inside each slot's 16-byte-aligned copy
-            const int offd = (int)(w0 & 1), offf = (int)(w0 & 3);
-            for (int i = threadIdx.x; i < nt; i += NT) {
-                double va[KK], vb[KK];
-                int soff = 0;
-#pragma unroll
-                for (int j = 0; j < KK; ++j) {
-                    if (j < NDJ) {
-                        const double* p = (const double*)(st + soff) + offd + i;
-                        va[j] = p[0];
-                        vb[j] = p[1];
-                        soff += lp.slot_elems * 8;
-                    } else {
-                        const float* p = (const float*)(st + soff) + offf + i;
-                        va[j] = (double)p[0];
-                        vb[j] = (double)p[1];
-                        soff += lp.slot_elems * 4;
-                    }
-                }
-#pragma unroll
-                for (int j = 0; j < KK; ++j) {
-                    double oa = 0.0, ob = 0.0;
-#pragma unroll
-                    for (int l = 0; l < KK; ++l) {
-                        oa = fma(wr[j * KK + l], va[l], oa);
-                        ob = fma(wr[KK * KK + j * KK + l], vb[l], ob);
-                    }
-                    double o = oa + ob;
-                    if (cp) o = vb[j];  // alpha == 0: exact copy (R4)
-                    if (j < NDJ) __stcs((double*)l_slot(dst, lay, j, t0 + i), o);
-                    else __stcs((float*)l_slot(dst, lay, j, t0 + i), __double2float_rn(o));
-                }
+            // window start inside each slot's 16-byte-aligned copy: (t0 - s - 1) mod 4, equal for all tiles
+            switch ((int)(w0 & 3)) {
+                case 0: line_consume_stage<KK, NDJ, 0>(st, lp.slot_elems, nt, N, t0, wr, cp, dst); break;
+                case 1: line_consume_stage<KK, NDJ, 1>(st, lp.slot_elems, nt, N, t0, wr, cp, dst); break;
+                case 2: line_consume_stage<KK, NDJ, 2>(st, lp.slot_elems, nt, N, t0, wr, cp, dst); break;
+                default: line_consume_stage<KK, NDJ, 3>(st, lp.slot_elems, nt, N, t0, wr, cp, dst); break;
             }
             __syncwarp();
             if (lane == 0) l_arrive(&empty[st_i]);

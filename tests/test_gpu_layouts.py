@@ -83,6 +83,38 @@ def test_table_II_mechanism_on_gpu(k):
     assert oracle.l2_norm_diff(out[0][0], out[k][0], 1.0 / N, k) > 10 * l2
 
 
+def test_weight_reuse_sequence():
+    """The library skips the weight build when a constant-shift sweep repeats the previous one's
+    (shift, extent).  A mixed sequence of repeated / changed shifts, dims, extents and fields must
+    still match the oracle step by step."""
+    from paper_1603_07008_b200 import Grid
+    k = 3
+    c = sldg_inputs.random_coeffs([16, 16, 12], k, 7)
+    g = Grid([16, 16, 12], k)
+    g.set_coeffs(c)
+    ref = oracle.round_layout(c, k, 1)
+    f2 = np.linspace(-3.3, 2.7, 16 * 16)
+    seq = [(0, 0.3, None, 0), (0, 0.3, None, 0), (1, 0.3, None, 0), (2, 0.3, None, 0), (2, 0.3, None, 0),
+           (2, 0.0, None, 0), (2, 0.0, None, 0), (0, 0.0, None, 0), (2, 0.0, f2, 0b011), (2, 0.0, None, 0),
+           (1, -1.75, None, 0), (0, -1.75, None, 0), (0, -1.75, None, 0)]
+    for dim, nu, fld, mask in seq:
+        if fld is None:
+            g.advect(dim, shift=nu)
+            ref = oracle.advect(ref, [16, 16, 12], k, dim, shift=nu, n_double=1)
+        else:
+            g.advect(dim, field=fld, field_mask=mask)
+            ref = oracle.advect(ref, [16, 16, 12], k, dim, field=fld, field_mask=mask, n_double=1)
+        got = g.get_coeffs()
+        K = k ** 3
+        d0 = np.max(np.abs(got[:, 0] - ref[:, 0]))
+        assert d0 <= 1e-13 * np.max(np.abs(ref[:, 0])), (dim, nu)
+        for q in range(1, K):
+            m = np.max(np.abs(ref[:, q]))
+            assert np.max(np.abs(got[:, q] - ref[:, q])) <= 8.0 * float(np.spacing(np.float32(m))), (dim, nu, q)
+        ref = got.copy()  # continue from the GPU state so that only this step's error is measured
+    g.destroy()
+
+
 def test_general_layout_rejected_in_multid():
     from paper_1603_07008_b200 import SldgError
     with pytest.raises(SldgError):

@@ -19,10 +19,8 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-import sldg_inputs  # noqa: E402
 from paper_1603_07008_b200 import Grid  # noqa: E402
 
 PAPER = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_tables.json")))
@@ -30,8 +28,7 @@ PAPER = json.load(open(os.path.join(ROOT, "tests", "golden", "paper_tables.json"
 
 def run(N, o, d, steps, reps, nu):
     g = Grid([N], o, precision=d)
-    c = sldg_inputs.random_coeffs([N], o, 1603)
-    g.set_coeffs(c)
+    g.fill_random(1603)
     stream = torch.cuda.ExternalStream(g.stream())
     for _ in range(5):
         g.advect(0, shift=nu)
@@ -48,10 +45,18 @@ def run(N, o, d, steps, reps, nu):
         g.sync()
         times.append(e0.elapsed_time(e1) / steps)
     ms = statistics.median(times)
+    # sweep kernel alone (events the library records around each sweep launch)
+    g.profile(True)
+    g.kernel_time(0, reset=True)
+    for _ in range(steps):
+        g.advect(0, shift=nu)
+    g.sync()
+    kms, kn, _ = g.kernel_time(0)
+    g.profile(False)
     kern = g.sweep_kernel(0)
     g.destroy()
     bytes_step = 2 * N * (8 * d + 4 * (o - d))
-    return ms, bytes_step / (ms * 1e-3) / 1e9, kern
+    return ms, bytes_step / (ms * 1e-3) / 1e9, kern, kms / kn, bytes_step / (kms / kn * 1e-3) / 1e9
 
 
 def main():
@@ -60,19 +65,22 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--nu", type=float, default=2.25)
+    ap.add_argument("--orders", default="2,4")
+    ap.add_argument("--doubles", default=None, help="comma list of d (default: o..0)")
     ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "round1", "paper_tables_b200.md"))
     args = ap.parse_args()
     torch.cuda.set_device(0)
     N = args.cells
     rows = []
-    for o in [2, 4]:
+    for o in [int(x) for x in args.orders.split(",")]:
         base = None
-        for d in range(o, -1, -1):
-            ms, gbs, kern = run(N, o, d, args.steps, args.reps, args.nu)
-            if d == o:
+        ds = range(o, -1, -1) if args.doubles is None else [int(x) for x in args.doubles.split(",")]
+        for d in ds:
+            ms, gbs, kern, kms, kgbs = run(N, o, d, args.steps, args.reps, args.nu)
+            if base is None:
                 base = ms
             rows.append({"o": o, "d": d, "ms": ms, "gbs": gbs, "gdofs": N * o / (ms * 1e-3) / 1e9,
-                         "speedup": base / ms, "memorydown": 8.0 * o / (8 * d + 4 * (o - d)), "kernel": kern})
+                         "kernel_ms": kms, "kernel_gbs": kgbs, "speedup": base / ms, "memorydown": 8.0 * o / (8 * d + 4 * (o - d)), "kernel": kern})
     paper = {}
     for key in ["table_III_cpu", "table_VI_k80_cell", "table_V_k80_smem"]:
         for r in PAPER[key]["rows"]:
@@ -83,14 +91,17 @@ def main():
              "(the paper's definition, pinned by its speedup identity, SURVEY 4).  Paper columns: "
              "Table III (2x Xeon E5-2630 v3) and Table VI (0.5x K80, thread per cell; Table V for o=2).",
              "",
-             "| o | # double d | B200 GB/s | B200 GDoF/s | B200 speedup vs d=o | memorydown | CPU GB/s (speedup) | K80 GB/s (speedup) | kernel |",
-             "|---|---|---|---|---|---|---|---|---|"]
+             "Step = one `sldg_advect` call (weight build + sweep launch, host enqueue included); the "
+             "kernel column is the sweep kernel alone (CUDA events around its launch).",
+             "",
+             "| o | # double d | B200 GB/s (step) | B200 GB/s (kernel) | B200 GDoF/s | B200 speedup vs d=o | memorydown | CPU GB/s (speedup) | K80 GB/s (speedup) | kernel |",
+             "|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
         p = paper.get((r["o"], r["d"]), {})
         cpu = p.get("table_III_cpu")
         k80 = p.get("table_VI_k80_cell") or p.get("table_V_k80_smem")
         fmt = lambda t: "--" if t is None else f"{t[2]} ({t[3] if t[3] is not None else '--'})"  # noqa: E731
-        lines.append(f"| {r['o']} | {r['d']} | {r['gbs']:.0f} | {r['gdofs']:.1f} | {r['speedup']:.2f} | "
+        lines.append(f"| {r['o']} | {r['d']} | {r['gbs']:.0f} | {r['kernel_gbs']:.0f} | {r['gdofs']:.1f} | {r['speedup']:.2f} | "
                      f"{r['memorydown']:.2f} | {fmt(cpu)} | {fmt(k80)} | {r['kernel']} |")
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     open(args.out, "w").write("\n".join(lines) + "\n")
