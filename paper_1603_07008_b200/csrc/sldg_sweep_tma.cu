@@ -546,16 +546,33 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
 
 // ============================================================================================
 // contiguous sweep (d = 0): R whole lines x GC coupled groups per stage.  Every consumer thread
-// owns cells of ONE line of the tile (R = NT / n0 lines of one cell per thread when n0 <= NT,
-// else R = 1 and n0 / NT cells per thread), so its weights are loaded once per tile.
-//   tensor maps (5D): {box0, L / box0, 1, plane, layer}, box {box0, cs / box0, 1, BP, 1},
+// owns kD0Tpt = 4 consecutive target cells of ONE line of the tile (R = 4 NT / n0 lines when
+// n0 <= 4 NT, else R = 1 and ceil(n0 / 4 NT) quads per thread), so its weights are loaded once
+// per tile, and the 5 source cells of its 4 targets (target r: A from cell r, B from cell r+1)
+// are read from shared memory and promoted once.  A layer's last tile may hold fewer than R
+// lines: its box reaches past the layer (TMA fills zeros, never read) and the spare threads idle.
+//   tensor maps (5D): {W, L / W, 1, plane, layer}, box {W, cs / W, 1, BP, 1},
 //   cs = R n0 cells per stage row: one box = BP consecutive planes of the tile's cells.
 // ============================================================================================
-// One coupled group.  sa / sb: the stage bytes of this cell's A- and B-source columns in the
-// group's first slot; slots are cs elements apart (CSC = compile-time cs when known, so the
-// shared-memory loads use immediate offsets).  CP: alpha == 0, exact copy of the B-source bits.
+constexpr int kD0Tpt = 4;
+
+// 4 outputs of one slot -> HBM (16-byte aligned: the quad starts at a multiple of 4 cells)
+__device__ __forceinline__ void st4(double* p, double a, double b, double c, double d)
+{
+    __stcs((double2*)p, make_double2(a, b));
+    __stcs((double2*)p + 1, make_double2(c, d));
+}
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d)
+{
+    __stcs((float4*)p, make_float4(a, b, c, d));
+}
+
+// One coupled group for the thread's 4 targets.  sp: the group's first slot in the stage; slots
+// are cs elements apart (CSC = compile-time cs when known, so the shared-memory loads use
+// immediate offsets); col[0..4]: stage columns of the 5 source cells.  CP: alpha == 0, exact
+// copy of the B-source bits.
 template <int KK, int PREC, bool MASSG, bool CP, int CSC>
-__device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, int cA, int cB, double*& om,
+__device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, const int* col, double*& om,
                                          float*& of, int64_t L, const double* wr)
 {
 #define SLDG_DBL(j) ((PREC == SLDG_FP64) || (MASSG && (j) == 0))
@@ -564,82 +581,87 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, in
 #pragma unroll
         for (int j = 0; j < KK; ++j) {
             if (SLDG_DBL(j)) {
-                __stcs(om, ((const double*)sp)[cB]);
+                const double* p = (const double*)sp;
+                st4(om, p[col[1]], p[col[2]], p[col[3]], p[col[4]]);
                 om += L;
                 sp += cs * 8;
             } else {
-                __stcs(of, ((const float*)sp)[cB]);
+                const float* p = (const float*)sp;
+                st4(of, p[col[1]], p[col[2]], p[col[3]], p[col[4]]);
                 of += L;
                 sp += cs * 4;
             }
         }
         return;
     }
-    double va[KK], vb[KK];
+    double v[KK][kD0Tpt + 1];
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
         if (SLDG_DBL(j)) {
-            va[j] = ((const double*)sp)[cA];
-            vb[j] = ((const double*)sp)[cB];
+            const double* p = (const double*)sp;
+#pragma unroll
+            for (int r = 0; r <= kD0Tpt; ++r) v[j][r] = p[col[r]];
             sp += cs * 8;
         } else {
-            va[j] = (double)((const float*)sp)[cA];
-            vb[j] = (double)((const float*)sp)[cB];
+            const float* p = (const float*)sp;
+#pragma unroll
+            for (int r = 0; r <= kD0Tpt; ++r) v[j][r] = (double)p[col[r]];
             sp += cs * 4;
         }
     }
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
-        // A- and B-parts as two independent FMA chains (k deep instead of 2k), then one add
-        double oa = 0.0, ob = 0.0;
+        double o[kD0Tpt];
 #pragma unroll
-        for (int l = 0; l < KK; ++l) {
-            oa = fma(wr[j * KK + l], va[l], oa);
-            ob = fma(wr[KK * KK + j * KK + l], vb[l], ob);
+        for (int r = 0; r < kD0Tpt; ++r) {
+            // A- and B-parts as two independent FMA chains (k deep instead of 2k), then one add
+            double oa = 0.0, ob = 0.0;
+#pragma unroll
+            for (int l = 0; l < KK; ++l) {
+                oa = fma(wr[j * KK + l], v[l][r], oa);
+                ob = fma(wr[KK * KK + j * KK + l], v[l][r + 1], ob);
+            }
+            o[r] = oa + ob;
         }
-        const double o = oa + ob;
         if (SLDG_DBL(j)) {
-            __stcs(om, o);
+            st4(om, o[0], o[1], o[2], o[3]);
             om += L;
         } else {
-            __stcs(of, __double2float_rn(o));
+            st4(of, __double2float_rn(o[0]), __double2float_rn(o[1]), __double2float_rn(o[2]),
+                __double2float_rn(o[3]));
             of += L;
         }
     }
 #undef SLDG_DBL
 }
 
-// all gc coupled groups of a stage for one target cell (columns cA, cB of the stage rows).
-// Mixed: om = mass of the cell, of = plane of slot q0 (or of slot 1 for the mass group);
-// fp64: om = slot q0 of the cell.
+// all gc coupled groups of a stage for the thread's quad of target cells.
+// Mixed: om = mass of the first cell, of = plane of slot q0 (or of slot 1 for the mass group);
+// fp64: om = slot q0 of the first cell.
 template <int KK, int PREC, bool MASSG, bool CP, int CSC>
-__device__ __forceinline__ void d0_consume_t(const unsigned char* sbase, int gc, int cs, int cA, int cB, double* om,
+__device__ __forceinline__ void d0_consume_t(const unsigned char* sbase, int gc, int cs, const int* col, double* om,
                                              float* of, int64_t L, const double* wr)
 {
     const unsigned char* sp = sbase;
     int gi = 0;
     if (MASSG) {
-        d0_group<KK, PREC, true, CP, CSC>(sp, cs, cA, cB, om, of, L, wr);
+        d0_group<KK, PREC, true, CP, CSC>(sp, cs, col, om, of, L, wr);
         gi = 1;
     }
-    // two groups per iteration: independent FMA chains for the scheduler to interleave
-    for (; gi + 1 < gc; gi += 2) {
-        d0_group<KK, PREC, false, CP, CSC>(sp, cs, cA, cB, om, of, L, wr);
-        d0_group<KK, PREC, false, CP, CSC>(sp, cs, cA, cB, om, of, L, wr);
-    }
-    if (gi < gc) d0_group<KK, PREC, false, CP, CSC>(sp, cs, cA, cB, om, of, L, wr);
+#pragma unroll 1
+    for (; gi < gc; ++gi) d0_group<KK, PREC, false, CP, CSC>(sp, cs, col, om, of, L, wr);
 }
 
 template <int KK, int PREC, bool MASSG>
-__device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, int cs, int cA, int cB, double* om,
+__device__ __forceinline__ void d0_consume(const unsigned char* sbase, int gc, int cs, const int* col, double* om,
                                            float* of, int64_t L, int cp, const double* wr)
 {
     if (cp) {
-        d0_consume_t<KK, PREC, MASSG, true, 0>(sbase, gc, cs, cA, cB, om, of, L, wr);
-    } else if (cs == 256) {
-        d0_consume_t<KK, PREC, MASSG, false, 256>(sbase, gc, cs, cA, cB, om, of, L, wr);
+        d0_consume_t<KK, PREC, MASSG, true, 0>(sbase, gc, cs, col, om, of, L, wr);
+    } else if (cs == 1024) {
+        d0_consume_t<KK, PREC, MASSG, false, 1024>(sbase, gc, cs, col, om, of, L, wr);
     } else {
-        d0_consume_t<KK, PREC, MASSG, false, 0>(sbase, gc, cs, cA, cB, om, of, L, wr);
+        d0_consume_t<KK, PREC, MASSG, false, 0>(sbase, gc, cs, col, om, of, L, wr);
     }
 }
 
@@ -674,23 +696,23 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
     const int64_t L = lay.L;
     const int R = pl.R, GC = pl.GC;
     const int64_t lines_per_layer = L / n0;
-    const int64_t nblk = lines_per_layer / R;
+    const int64_t nblk = (lines_per_layer + R - 1) / R;  // tiles per layer (the last may be partial)
     const int64_t nlay = le - lb;
     const int64_t ntiles = nblk * nlay;
     const int G = lay.K / KK;
-    const int NT = NC * 32;
-    const int cell_stride = R * n0;  // elements of one slot in a stage
-    const int box0 = pl.W;           // first box dim (cells)
-    const int BP = GC * KK;          // planes per box
+    const int NQ = NC * 32 * kD0Tpt;  // cells covered by one pass of the consumer threads
+    const int cell_stride = R * n0;    // elements of one slot in a stage
+    const int box0 = pl.W;             // first box dim (cells)
+    const int BP = GC * KK;            // planes per box
     const uint64_t pol = policy_evict_first();
     // this thread's line of the tile and first cell
-    const int my_r = (n0 <= NT) ? (int)threadIdx.x / n0 : 0;
-    const int my_c0 = (n0 <= NT) ? (int)threadIdx.x % n0 : (int)threadIdx.x;
-    const int ncell = (n0 <= NT) ? 1 : n0 / NT;
-    const bool has_cell = !producer && my_r < R;
+    const int q4 = (int)threadIdx.x * kD0Tpt;
+    const int my_r = (n0 <= NQ) ? q4 / n0 : 0;
+    const int my_c0 = (n0 <= NQ) ? q4 % n0 : q4;
+    const int nquad = (n0 <= NQ) ? 1 : (n0 + NQ - 1) / NQ;
 
     // Line data (A, B, i* mod n, copy flag) travels with the tile's first stage: the producer
-    // bulk-copies the R packed line records (Weights::rec, 16(k^2+1) bytes each) into the
+    // bulk-copies the tile's packed line records (Weights::rec, 16(k^2+1) bytes each) into the
     // stage's record area, so no thread waits on a global load at a tile boundary and no
     // registers hold a prefetch.
     const int recw = 2 * KK * KK + 2;  // doubles per record
@@ -705,6 +727,8 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
         const int64_t layer = lb + tile / nblk;
         const int64_t layerp = lay.pad + layer;
         const int64_t inner_base = blk * R * (int64_t)n0;  // first cell of the tile's first line
+        const int rv = (lines_per_layer - blk * R < R) ? (int)(lines_per_layer - blk * R) : R;  // lines in this tile
+        const bool has_cell = !producer && my_r < rv;
         for (int g0 = 0; g0 < G; g0 += GC) {
             const int gc = (G - g0) < GC ? (G - g0) : GC;
             const int s = it % S;
@@ -717,7 +741,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                     mbar_wait(&empty[s], ph ^ 1);
                     const uint32_t es = (PREC == SLDG_FP64) ? 8u : 4u;
                     uint32_t bytes = (uint32_t)cell_stride * (BP * es + (massg ? 8u : 0u));
-                    if (g0 == 0) bytes += (uint32_t)(R * recw * 8);
+                    if (g0 == 0) bytes += (uint32_t)(rv * recw * 8);
                     mbar_expect_tx(&full[s], bytes);
                     const int c1 = (int)(inner_base / box0);
                     if (massg) {
@@ -728,7 +752,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                         tma_5d(st, &tmaps.f[0], 0, c1, 0, plane0, (int)layerp, &full[s], pol);
                     }
                     if (g0 == 0) {
-                        for (int r = 0; r < R; ++r) {  // the tile's line records
+                        for (int r = 0; r < rv; ++r) {  // the tile's line records
                             int64_t f = 0;
                             if (sw.fmask) {  // 32-bit index math: this thread feeds the whole CTA
                                 int64_t idx[kMaxDim];
@@ -759,13 +783,18 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                     my_cp = (int)__double_as_longlong(rp[2 * KK * KK + 1]);
                 }
                 if (has_cell) {
-                    for (int ci = 0; ci < ncell; ++ci) {
-                        const int cc = my_c0 + ci * NT;  // column (target cell within the line)
-                        int cB = cc - (int)my_s;
-                        if (cB < 0) cB += n0;
-                        int cA = cB - 1;
-                        if (cA < 0) cA += n0;
+                    for (int ci = 0; ci < nquad; ++ci) {
+                        const int cc = my_c0 + ci * NQ;  // first target cell of the quad within the line
+                        if (cc >= n0) break;
                         const int row0 = my_r * n0;
+                        int col[kD0Tpt + 1];
+                        int c = cc - (int)my_s - 1;  // A-source of target cc (i* mod n in [0, n0))
+                        if (c < 0) c += n0;
+#pragma unroll
+                        for (int r = 0; r <= kD0Tpt; ++r) {
+                            col[r] = row0 + c;
+                            c = (c + 1 == n0) ? 0 : c + 1;
+                        }
                         const int64_t tin = inner_base + row0 + cc;
                         const int q0 = g0 * KK;
                         double* om;
@@ -777,9 +806,9 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                             of = dst.pl + toff_f<PREC>(lay, layerp, tin) + (massg ? 0 : (int64_t)(q0 - 1) * L);
                         }
                         if (massg)
-                            d0_consume<KK, PREC, true>(st, gc, cell_stride, row0 + cA, row0 + cB, om, of, L, my_cp, wr);
+                            d0_consume<KK, PREC, true>(st, gc, cell_stride, col, om, of, L, my_cp, wr);
                         else
-                            d0_consume<KK, PREC, false>(st, gc, cell_stride, row0 + cA, row0 + cB, om, of, L, my_cp, wr);
+                            d0_consume<KK, PREC, false>(st, gc, cell_stride, col, om, of, L, my_cp, wr);
                     }
                 }
                 __syncwarp();
@@ -866,16 +895,12 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
     const int64_t layers_alloc = lay.layers + 2 * lay.pad;
     if (lay.L > (int64_t)1 << 31 || layers_alloc > 65535) return false;
     if (sw.dim == 0) {
-        int64_t R;
-        if (n0 <= NT) {
-            if (NT % n0 != 0) return false;
-            R = NT / n0;
-        } else {
-            if (n0 % NT != 0) return false;
-            R = 1;
-        }
+        // 4 consecutive targets per consumer thread (kD0Tpt): R lines of n0 cells per tile
+        const int64_t NQ = (int64_t)NT * 4;
         const int64_t lines = lay.L / n0;
-        if (lines % R != 0) return false;
+        int64_t R = (n0 <= NQ) ? std::min<int64_t>(NQ / n0, lines) : 1;
+        while (R > 1 && (R * n0) % 16 != 0) --R;  // stage slots stay 64-byte multiples
+        if ((R * n0) % 16 != 0) return false;
         const int64_t cs = R * n0;
         const int64_t group_bytes = cs * bpc_max;  // one coupled group of the tile, worst case
         const int G = lay.K / k;
@@ -889,8 +914,12 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
         if (GC * k > 256) return false;
         pl->R = (int)R;
         pl->GC = GC;
-        pl->W = (int)std::min<int64_t>(256, cs);  // first box dim
-        if (cs % pl->W != 0 || cs / pl->W > 256 || lay.L % pl->W != 0) return false;
+        // first box dim: the largest power of two <= 256 dividing cs and L (tiles start at
+        // multiples of cs, so at multiples of W)
+        int W = 256;
+        while (W > 16 && (cs % W != 0 || lay.L % W != 0)) W >>= 1;
+        if (cs % W != 0 || lay.L % W != 0 || cs / W > 256) return false;
+        pl->W = W;
         const int es = (lay.prec == SLDG_FP64) ? 8 : 4;
         // stage: [mass (mixed mass group)] + GC*k planes (the mass group's box holds one spare plane)
         // + the tile's R packed line records at the end (16-byte aligned: 16(k^2+1) bytes each)
@@ -1053,7 +1082,7 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
     int64_t ntiles;
     const int per_sm = pl.ctas;  // CTAs per SM the plan sized shared memory for
     if (sw.dim == 0) {
-        ntiles = (lay.L / lay.n[0] / pl.R) * (le - lb);
+        ntiles = ((lay.L / lay.n[0] + pl.R - 1) / pl.R) * (le - lb);
         auto kern = (pl.ctas == 2) ? sweep_d0_tma<KK, PREC, 2> : sweep_d0_tma<KK, PREC, 1>;
         static bool attr_set[3] = {false, false, false};  // once per instantiation: full opt-in carveout
         if (!attr_set[pl.ctas]) {
