@@ -20,13 +20,6 @@
 
 using namespace sldg;
 
-struct sldg_grid_s : public Grid {
-    cudaStream_t comm_stream = nullptr;
-    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
-    int64_t* d_range = nullptr;
-    bool halo_mode = false;  // sweeps along the layer dim read halo layers (sharded, or forced)
-};
-
 namespace {
 
 thread_local std::string g_last_error;
@@ -389,6 +382,8 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
 }
 
 }  // namespace
+
+sldg_status sldg::set_error(sldg_status st, const std::string& msg) { return fail(st, msg); }
 
 extern "C" {
 

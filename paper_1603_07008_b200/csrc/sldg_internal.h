@@ -125,6 +125,9 @@ struct Grid {
     int64_t launches = 0;
 };
 
+// records msg as sldg_last_error() and returns st (sldg_abi.cu)
+sldg_status set_error(sldg_status st, const std::string& msg);
+
 // ---- kernel launchers (sldg_kernels.cu) -------------------------------------------------
 cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field, double shift,
                            int64_t n_entries, Weights& w, int* d_err, cudaStream_t s);
@@ -168,3 +171,11 @@ cudaError_t launch_sweep_tma(const Layout& lay, const Sweep& sw, const Arrays& s
                              int64_t layer_begin, int64_t layer_end, const TmaPlan& pl, cudaStream_t s);
 
 }  // namespace sldg
+
+// The opaque ABI handle: the grid plus the distributed-sweep state (sldg_abi.cu).
+struct sldg_grid_s : public sldg::Grid {
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
+    int64_t* d_range = nullptr;
+    bool halo_mode = false;  // sweeps along the layer dim read halo layers (sharded, or forced)
+};

@@ -26,7 +26,8 @@ EXPORTS = [
     "sldg_get_stream", "sldg_memory_bytes", "sldg_last_error", "sldg_fill_random",
     "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
     "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_halo_plan", "sldg_layer_owner",
-    "sldg_sweep_kernel",
+    "sldg_sweep_kernel", "sldg_vp_create", "sldg_vp_destroy", "sldg_vp_density", "sldg_vp_field",
+    "sldg_vp_step",
 ]
 
 
@@ -87,6 +88,11 @@ def lib():
         "sldg_halo_widths": [i64, i64, i64p, i64p],
         "sldg_halo_plan": [i64, ctypes.c_int, ctypes.c_int, i64, i64, i64, i64p, i64, i64p],
         "sldg_layer_owner": [i64, ctypes.c_int, i64, ctypes.POINTER(ctypes.c_int), i64p],
+        "sldg_vp_create": [vp, ctypes.c_int, ctypes.POINTER(vp)],
+        "sldg_vp_destroy": [vp],
+        "sldg_vp_density": [vp, dp],
+        "sldg_vp_field": [vp, dp, dp, dp, dp],
+        "sldg_vp_step": [vp, ctypes.c_double, dp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -267,3 +273,54 @@ class Grid:
 
     def sweep_kernel(self, dim: int) -> str:
         return lib().sldg_sweep_kernel(self.h, int(dim)).decode()
+
+
+class VlasovPoisson:
+    """Vlasov-Poisson driver on a Grid whose dims are [x_1..x_dx, v_1..v_dx] (sldg_vp_*; NEXT-2)."""
+
+    def __init__(self, grid: "Grid", dx: int):
+        self.grid = grid
+        self.dx = int(dx)
+        self.k = grid.k
+        self.nx = [int(n) for n in grid.cells[: self.dx]]
+        self.Nx = int(np.prod(self.nx))
+        self.Kx = self.k ** self.dx
+        h = ctypes.c_void_p()
+        _check(lib().sldg_vp_create(grid.h, self.dx, ctypes.byref(h)))
+        self.h = h
+
+    def destroy(self):
+        if self.h:
+            lib().sldg_vp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+    def density(self) -> np.ndarray:
+        out = np.empty((self.Nx, self.Kx))
+        _check(lib().sldg_vp_density(self.h, _dp(out)))
+        return out
+
+    def field(self, rho=None):
+        """(E at x-cell centres [dx, Nx], E Legendre coefficients [Nx, k+1] (dx = 1) or None,
+        electric energy); from the grid's f, or from a given density [Nx, k^dx]."""
+        e = np.empty((self.dx, self.Nx))
+        coef = np.empty((self.Nx, self.k + 1)) if self.dx == 1 else None
+        w = np.empty(1)
+        r = None if rho is None else np.ascontiguousarray(rho, dtype=np.float64).reshape(-1)
+        _check(lib().sldg_vp_field(self.h, None if r is None else _dp(r), _dp(e),
+                                   None if coef is None else _dp(coef), _dp(w)))
+        return e, coef, float(w[0])
+
+    def step(self, dt: float, energy: bool = False):
+        """One Strang step; returns the mid-step electric energy when energy=True."""
+        if energy:
+            w = np.empty(1)
+            _check(lib().sldg_vp_step(self.h, float(dt), _dp(w)))
+            return float(w[0])
+        _check(lib().sldg_vp_step(self.h, float(dt), None))
+        return None

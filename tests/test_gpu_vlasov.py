@@ -1,0 +1,167 @@
+"""GPU parity of the Vlasov-Poisson driver (sldg_vp_*, NEXT-2, readings V1-V6)
+against oracle/vlasov.py, plus the Landau damping rate from the dispersion relation."""
+import numpy as np
+import pytest
+
+import oracle
+import sldg_inputs
+from oracle import vlasov as ovp
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+
+
+def _mk(dims, k, dx, precision="mixed", **kw):
+    from paper_1603_07008_b200 import Grid, VlasovPoisson
+    lo = [0.0] * dx + [-6.0] * dx
+    hi = [4 * np.pi] * dx + [6.0] * dx
+    g = Grid(dims, k, lo=lo, hi=hi, precision=precision, **kw)
+    return g, VlasovPoisson(g, dx), lo, hi
+
+
+def _nd(precision, K):
+    return 1 if precision == "mixed" else K
+
+
+def _close(got, ref, rel=1e-13, tag=""):
+    got, ref = np.asarray(got), np.asarray(ref)
+    scale = max(np.max(np.abs(ref)), 1e-300)
+    d = np.max(np.abs(got - ref))
+    assert d <= rel * scale, f"{tag}: |d| = {d:.3e} > {rel:.0e} * {scale:.3e}"
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+@pytest.mark.parametrize("dims,k,dx", [([12, 20], 3, 1), ([64, 7], 4, 1), ([6, 5, 4, 7], 2, 2), ([8, 4, 6, 6], 3, 2)])
+def test_density_parity(dims, k, dx, precision):
+    g, vp, lo, hi = _mk(dims, k, dx, precision)
+    K = k ** len(dims)
+    c = sldg_inputs.random_coeffs(dims, k, 11)
+    g.set_coeffs(c)
+    ref = ovp.density(oracle.round_layout(c, K, _nd(precision, K)), dims, k, dx, lo, hi)
+    _close(vp.density(), ref, tag="density")
+    vp.destroy()
+    g.destroy()
+
+
+@pytest.mark.parametrize("n,k", [(50, 3), (7, 1), (300, 4), (1000, 2)])
+def test_poisson_1d_parity(n, k):
+    g, vp, lo, hi = _mk([n, 4], k, 1, "fp64")
+    rng = np.random.default_rng(n)
+    rho = rng.standard_normal((n, k))
+    e, coef, w = vp.field(rho)
+    ref = ovp.poisson_1d(rho, n, hi[0] - lo[0])
+    _close(coef, ref, tag="E coefficients")
+    _close(e[0], ovp.field_centres_1d(ref), tag="E centres")
+    assert abs(w - ovp.energy_1d(ref, (hi[0] - lo[0]) / n)) <= 1e-13 * ovp.energy_1d(ref, (hi[0] - lo[0]) / n)
+    vp.destroy()
+    g.destroy()
+
+
+@pytest.mark.parametrize("n1,n2", [(12, 10), (9, 16), (64, 64), (5, 3)])
+def test_poisson_2d_parity(n1, n2):
+    g, vp, lo, hi = _mk([n1, n2, 2, 2], 2, 2, "fp64")
+    rng = np.random.default_rng(n1 * 100 + n2)
+    rho = rng.standard_normal((n1 * n2, 4))
+    e, coef, w = vp.field(rho)
+    assert coef is None
+    e1, e2 = ovp.poisson_2d(rho[:, 0], n1, n2, hi[0] - lo[0], hi[1] - lo[1])
+    _close(e[0], e1, rel=1e-12, tag="E1")
+    _close(e[1], e2, rel=1e-12, tag="E2")
+    wr = ovp.energy_2d(e1, e2, (hi[0] - lo[0]) / n1, (hi[1] - lo[1]) / n2)
+    assert abs(w - wr) <= 1e-12 * wr
+    vp.destroy()
+    g.destroy()
+
+
+@pytest.mark.parametrize("dims,k,dx,steps", [([32, 64], 3, 1, 4), ([16, 12, 10, 8], 2, 2, 2)])
+@pytest.mark.parametrize("force_halo", [False, True])
+def test_strang_step_parity(dims, k, dx, steps, force_halo):
+    """Each step compared with the oracle step started from the GPU state (only that step's
+    rounding differences are measured); Landau-type data with a strong perturbation so that the
+    field and the v-sweeps are far from trivial."""
+    kw = dict(force_halo=True, max_halo=3) if force_halo else {}
+    g, vp, lo, hi = _mk(dims, k, dx, "mixed", **kw)
+    K = k ** len(dims)
+    kinds = ["x"] * dx + ["v"] * dx
+    terms = sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=0.3, kappa=0.5)
+    c = sldg_inputs.assemble_separable(terms, dims, k)
+    g.set_coeffs(c)
+    cur = g.get_coeffs()
+    for s in range(steps):
+        w = vp.step(0.4, energy=True)
+        got = g.get_coeffs()
+        ref, _, wref = ovp.strang_step(cur, dims, k, dx, lo, hi, 0.4, n_double=1)
+        assert abs(w - wref) <= 1e-12 * wref, (s, w, wref)
+        d0 = np.max(np.abs(got[:, 0] - ref[:, 0]))
+        assert d0 <= 1e-13 * np.max(np.abs(ref[:, 0])), (s, d0)
+        for q in range(1, K):
+            m = np.max(np.abs(ref[:, q]))
+            assert np.max(np.abs(got[:, q] - ref[:, q])) <= 8.0 * float(np.spacing(np.float32(m))) + 1e-30, (s, q)
+        cur = got
+    vp.destroy()
+    g.destroy()
+
+
+def _landau_gamma(kappa):
+    import math
+    from scipy.special import wofz
+
+    def eps(w):
+        z = w / (math.sqrt(2) * kappa)
+        return 1 + (1 + z * 1j * math.sqrt(math.pi) * wofz(z)) / kappa ** 2
+    w = 1.4 - 0.15j
+    for _ in range(50):
+        w = w - eps(w) / ((eps(w + 1e-7) - eps(w - 1e-7)) / 2e-7)
+    return w.imag
+
+
+def _rate(ws, dt):
+    w = np.asarray(ws)
+    t = dt * np.arange(1, len(w) + 1)
+    pk = [i for i in range(1, len(w) - 1) if w[i] > w[i - 1] and w[i] >= w[i + 1] and 1.0 < t[i] < 18.0]
+    return np.polyfit(t[pk], np.log(w[pk]), 1)[0] / 2, len(pk)
+
+
+@pytest.mark.parametrize("dims,k,dx", [([32, 128], 3, 1), ([32, 32, 64, 64], 2, 2)])
+def test_landau_damping_on_gpu(dims, k, dx):
+    """Weak Landau damping (eps = 0.01, kappa = 0.5): the electric energy decays at twice the
+    dispersion-relation rate (within 3%), and mass is conserved to fp64 accuracy."""
+    from paper_1603_07008_b200 import Grid, VlasovPoisson
+    lo = [0.0] * dx + [-6.0] * dx
+    hi = [2 * np.pi / 0.5] * dx + [6.0] * dx
+    g = Grid(dims, k, lo=lo, hi=hi, precision="mixed")
+    vp = VlasovPoisson(g, dx)
+    kinds = ["x"] * dx + ["v"] * dx
+    g.fill_separable(sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=0.01, kappa=0.5))
+    m0 = g.mass()
+    ws = [vp.step(0.1, energy=True) for _ in range(190)]
+    gamma, npk = _rate(ws, 0.1)
+    want = _landau_gamma(0.5)
+    assert npk >= 4
+    assert abs(gamma - want) <= 0.03 * abs(want), (gamma, want)
+    assert abs(g.mass() - m0) / m0 <= 1e-12
+    vp.destroy()
+    g.destroy()
+
+
+def test_vp_rejects_bad_grids():
+    from paper_1603_07008_b200 import Grid, SldgError, VlasovPoisson
+    g = Grid([8, 8, 8], 2)
+    with pytest.raises(SldgError):
+        VlasovPoisson(g, 1)
+    with pytest.raises(SldgError):
+        VlasovPoisson(g, 2)
+    g.destroy()
+    g = Grid([16], 2, precision=1)
+    with pytest.raises(SldgError):
+        VlasovPoisson(g, 1)
+    g.destroy()
