@@ -209,6 +209,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--compare-fp64", action=argparse.BooleanOptionalAction, default=True,
                     help="also time the all-fp64 layout on a slab of the workload (mixed_vs_fp64)")
+    ap.add_argument("--vlasov", action=argparse.BooleanOptionalAction, default=True,
+                    help="also time the Vlasov-Poisson Strang step (NEXT-2) on the same grid")
     ap.add_argument("--sweeps", default=None, help="comma list of dims to run (default: all)")
     ap.add_argument("--dims", default=None, help="override grid extents (profiling slabs), e.g. 128,128,128,16")
     args = ap.parse_args()
@@ -370,15 +372,57 @@ def main():
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+    vp_res = None
+    if args.vlasov and world == 1 and args.sweeps is None:
+        vp_res = time_vlasov(g, stream, dims, kinds, k)
     g.destroy()
     del dev_fields
     if rank == 0:
+        if vp_res is not None:
+            out["vlasov_poisson_step"] = vp_res
         if args.compare_fp64 and world == 1:
             out["mixed_vs_fp64"] = compare_precisions(args, dims, kinds, k)
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def time_vlasov(g, stream, dims, kinds, k, steps=3, dt=0.1):
+    """NEXT-2: the Vlasov-Poisson Strang step (x sweeps dt/2, density, field, v sweeps dt,
+    x sweeps dt/2; sldg_vp_step) on the benchmark grid, and the density + field solve alone.
+    Device time (CUDA events on the grid stream)."""
+    import torch
+
+    from paper_1603_07008_b200 import VlasovPoisson
+
+    dx = kinds.count("x")
+    vp = VlasovPoisson(g, dx)
+    vp.step(dt)  # warm-up (also builds the tensor maps of every sweep)
+    vp.field_async()
+    g.sync()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    with torch.cuda.stream(stream):
+        ev[0].record(stream)
+    for _ in range(steps):
+        vp.step(dt)
+    with torch.cuda.stream(stream):
+        ev[1].record(stream)
+    for _ in range(steps):
+        vp.field_async()
+    with torch.cuda.stream(stream):
+        ev[2].record(stream)
+    g.sync()
+    step_ms = ev[0].elapsed_time(ev[1]) / steps
+    field_ms = ev[1].elapsed_time(ev[2]) / steps
+    cells, K = int(np.prod(dims)), k ** len(dims)
+    w = vp.step(dt, energy=True)
+    vp.destroy()
+    return {"ms_per_step": step_ms, "sweeps_per_step": 3 * dx, "density_and_field_ms": field_ms,
+            "field_share_of_step": field_ms / step_ms,
+            "gdofs_per_sweep": 3 * dx * cells * K / (step_ms * 1e-3) / 1e9,
+            "electric_energy": w, "dt": dt,
+            "field_solver": "1D: exact DG antiderivative (V3)" if dx == 1 else "2D: spectral on cell means (V4)"}
 
 
 def compare_precisions(args, dims, kinds, k):

@@ -316,6 +316,10 @@ class VlasovPoisson:
                                    None if coef is None else _dp(coef), _dp(w)))
         return e, coef, float(w[0])
 
+    def field_async(self):
+        """density + field solve of the grid's f into device buffers only (no host copy)."""
+        _check(lib().sldg_vp_field(self.h, None, None, None, None))
+
     def step(self, dt: float, energy: bool = False):
         """One Strang step; returns the mid-step electric energy when energy=True."""
         if energy:

@@ -78,6 +78,9 @@ CASES = [
     ([8, 4, 6, 5], 3),
     ([40, 3, 1, 7], 2),
     ([12, 5, 4, 3, 2], 2),
+    # inner sweeps with < 256 cells below d: tiles of HC = 256 / M_lo hi values (dim 1 here)
+    ([64, 16, 8, 6], 2),
+    ([32, 8, 16, 4], 3),
 ]
 
 
