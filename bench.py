@@ -360,6 +360,7 @@ def main():
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                          "kernel": f"{g.sweep_kernel(dom)} (sweep along dim {dom})",
                          "peak_source": peak_src,
+                         "frac_of_spec_8000": (achieved / 8000.0) if achieved else None,
                          "bytes_per_launch": d_bytes / d_n if d_n else None,
                          "avg_launch_ms": d_ms / d_n if d_n else None},
             "sweeps": {str(d): {"ms_per_launch": per_dim[d][0] / max(1, per_dim[d][1]),
