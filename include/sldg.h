@@ -94,6 +94,9 @@ typedef struct {
  * neighbour is the rank itself: halo layers are device copies).  Exercises the exact halo
  * addressing of multi-GPU runs on one GPU; no NCCL communicator is needed. */
 #define SLDG_DIST_FORCE_HALO 1
+/* Every sweep along the layer dim takes the transpose path (testing on one GPU; see
+ * sldg_transpose_plan).  Implies the halo layout. */
+#define SLDG_DIST_FORCE_TRANSPOSE 2
 
 /* Create a grid (zero-filled).  k in 1..SLDG_MAX_K coefficients per dim (the paper's order
  * o = p+1).  dist may be NULL (single GPU).  The device is the caller's current
@@ -124,7 +127,8 @@ sldg_status sldg_get_coeffs(sldg_grid g, double* dst, int64_t first_cell, int64_
  * i_e * prod_{e' in mask, e' < e} n_e' over GLOBAL indices; unmasked perpendicular dims
  * broadcast (per-line variable CFL).  Errors (EINVAL, no state change): dim out
  * of range, bit `dim` set in field_mask, mask bits >= D, non-finite or |nu| >= 2^62 entry
- * (S:211).  ENOTSUP: sharded sweep whose halo exceeds max_halo.  Asynchronous. */
+ * (S:211).  A sharded sweep whose halo exceeds max_halo (or would move more data than a
+ * re-shard) takes the transpose path (sldg_transpose_plan).  Asynchronous. */
 sldg_status sldg_advect(sldg_grid g, int dim, double shift, const double* field, uint32_t field_mask);
 /* Same, with the field already resident in DEVICE memory (d_field, fp64, same indexing).
  * Entries are validated on the device: a non-finite entry leaves its lines unchanged and
@@ -190,6 +194,19 @@ sldg_status sldg_halo_plan(int64_t n, int world, int rank, int64_t pad, int64_t 
 /* Owner rank and local index of global layer `layer` in a balanced block split of n over
  * world ranks. */
 sldg_status sldg_layer_owner(int64_t n, int world, int64_t layer, int* owner, int64_t* local);
+/* Host-only plan of the TRANSPOSE path of a sweep along the sharded dim D-1:
+ * taken when the halo exceeds max_halo, or when the halo would move more than the transpose
+ * (left + right > 2 n_local (P-1)/P).  The slab dim D-2 (extent n_slab) is block-split over
+ * the ranks like the layer dim (extent n_outer); rank r sends to every rank p its own layers
+ * restricted to p's slab, receives from p p's layers restricted to r's slab (whole lines along
+ * D-1 for its slab), sweeps them locally with periodic wrap, and returns them the same way.
+ * out[8 p + 0..3] = {send layer first, send layer count, send slab first, send slab count},
+ * out[8 p + 4..7] = {recv layer first, recv layer count, recv slab first, recv slab count}
+ * for p = 0..world-1 (out holds 8 * world int64).  The forward and inverse messages of
+ * sldg_advect follow exactly this plan (inverse = the same pairs reversed). */
+sldg_status sldg_transpose_plan(int64_t n_outer, int64_t n_slab, int world, int rank, int64_t* out);
+/* Number of sweeps of this handle that took the transpose path. */
+sldg_status sldg_transpose_count(sldg_grid g, int64_t* n);
 
 /* ---- Vlasov-Poisson driver around the sweep (NEXT-2, readings V1-V6) -------
  * The model is the paper's: d_t f + v.grad_x f + E(x).grad_v f = 0, reduced by

@@ -155,8 +155,10 @@ cudaEvent_t pool_event(sldg_grid g)
 }
 
 // Launch one sweep kernel over local layers [lb, le) with optional profiling events.
-sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arrays& dst, int64_t lb, int64_t le)
+sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arrays& dst, int64_t lb, int64_t le,
+                      const Layout* lay = nullptr)
 {
+    const Layout& LY = lay ? *lay : g->lay;
     if (le <= lb) return SLDG_OK;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (g->profile) {
@@ -165,12 +167,12 @@ sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arr
         CU(cudaEventRecord(e0, g->stream));
     }
     int nl = 0;
-    CU(launch_sweep(g->lay, sw, src, dst, lb, le, g->stream, &nl));
+    CU(launch_sweep(LY, sw, src, dst, lb, le, g->stream, &nl));
     g->launches += nl;
     if (g->profile) {
         CU(cudaEventRecord(e1, g->stream));
         g->ev_pairs.push_back({e0, e1});
-        g->ev_bytes.push_back(2.0 * (double)bytes_per_cell(g->lay) * (double)((le - lb) * g->lay.L));
+        g->ev_bytes.push_back(2.0 * (double)bytes_per_cell(LY) * (double)((le - lb) * LY.L));
         g->ev_dim.push_back(sw.dim);
     }
     return SLDG_OK;
@@ -272,6 +274,175 @@ sldg_status halo_exchange(sldg_grid g, const Arrays& a, int64_t left, int64_t ri
     return SLDG_OK;
 }
 
+// ---- transpose path of a sweep along the sharded dim (SURVEY 8(e) "When to transpose") ------
+// Used when the halo would not fit the pad layers or would move more than the transpose
+// (left + right > 2 n_local (P-1)/P).  The slab dim e = D-2 is block-split over the ranks like
+// the layer dim: rank r receives, from every rank p, p's layers restricted to r's slab
+// [a_r, a_r + s_r) of dim e -- a contiguous inner range of every plane -- so it holds whole lines
+// along D-1 for its slab, sweeps them locally (periodic, no halo), and sends them back.
+struct TrPart {
+    int64_t send_layer_first, send_layer_count, send_slab_first, send_slab_count;
+    int64_t recv_layer_first, recv_layer_count, recv_slab_first, recv_slab_count;
+};
+
+std::vector<TrPart> transpose_plan(int64_t n_outer, int64_t n_slab, int world, int rank)
+{
+    std::vector<TrPart> ps(world);
+    int64_t f_r, c_r, a_r, s_r;
+    split(n_outer, world, rank, &f_r, &c_r);
+    split(n_slab, world, rank, &a_r, &s_r);
+    for (int p = 0; p < world; ++p) {
+        int64_t f_p, c_p, a_p, s_p;
+        split(n_outer, world, p, &f_p, &c_p);
+        split(n_slab, world, p, &a_p, &s_p);
+        ps[p] = {f_r, c_r, a_p, s_p, f_p, c_p, a_r, s_r};
+    }
+    return ps;
+}
+
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double shift, int64_t n_entries,
+                            const Arrays& src, const Arrays& dst)
+{
+    const Layout& L = g->lay;
+    const int D = L.D, e = D - 2, P = g->world, r = g->rank;
+    const int64_t Mp = L.S[e];
+    const std::vector<TrPart> plan = transpose_plan(L.n[D - 1], L.n[e], P, r);
+    const int64_t nl = L.layers, nd = L.nd, nf = L.K - L.nd;
+    // slab layout: this rank's slab of dim e, all layers, no pad
+    Layout T = L;
+    T.n[e] = plan[r].recv_slab_count;
+    T.L = Mp * T.n[e];
+    T.layers = L.n[D - 1];
+    T.first_layer = 0;
+    T.pad = 0;
+    T.cells = T.layers * T.L;
+    const size_t tb = align256(array_alloc_bytes(T));
+    // message blocks (this rank's layers x slab p), per peer: fp64 part then fp32 part
+    std::vector<size_t> boff(P + 1, 0);
+    for (int p = 0; p < P; ++p) {
+        const int64_t len = plan[p].send_slab_count * Mp;
+        boff[p + 1] = boff[p] + align256((size_t)(nl * nd * len) * 8) + align256((size_t)(nl * nf * len) * 4);
+    }
+    const size_t need = 2 * tb + boff[P];
+    if (g->t_bytes < need) {
+        CU(cudaStreamSynchronize(g->stream));
+        cudaFree(g->t_alloc);
+        g->t_alloc = nullptr;
+        g->t_bytes = 0;
+        CU(cudaMalloc(&g->t_alloc, need));
+        g->t_bytes = need;
+    }
+    char* tbase = (char*)g->t_alloc;
+    const Arrays Tin = arrays_of(T, tbase), Tout = arrays_of(T, tbase + tb);
+    char* stage_fwd = (char*)g->alloc[1 - g->cur];  // dst array memory: overwritten by the unpack at the end
+    char* stage_inv = tbase + 2 * tb;
+    auto bm = [&](char* base, int p) { return (double*)(base + boff[p]); };
+    auto bf = [&](char* base, int p) {
+        return (float*)(base + boff[p] + align256((size_t)(nl * nd * plan[p].send_slab_count * Mp) * 8));
+    };
+    const int64_t lenr = plan[r].recv_slab_count * Mp;
+    ncclComm_t comm = (ncclComm_t)g->comm;
+    cudaStream_t st = g->stream;
+    // forward: pack, exchange, self copy
+    for (int p = 0; p < P; ++p) {
+        CU(launch_tr_block(L, src, nl, plan[p].send_slab_first * Mp, plan[p].send_slab_count * Mp, bm(stage_fwd, p),
+                           bf(stage_fwd, p), true, st));
+        g->launches += 1;
+    }
+    if (P > 1) {
+        NC(ncclGroupStart());
+        for (int p = 0; p < P; ++p) {
+            if (p == r) continue;
+            const int64_t len = plan[p].send_slab_count * Mp;
+            if (nl * nd * len) NC(ncclSend(bm(stage_fwd, p), (size_t)(nl * nd * len), ncclFloat64, p, comm, st));
+            if (nl * nf * len) NC(ncclSend(bf(stage_fwd, p), (size_t)(nl * nf * len), ncclFloat32, p, comm, st));
+            const int64_t rf = plan[p].recv_layer_first, rc = plan[p].recv_layer_count;
+            if (rc * nd * lenr) NC(ncclRecv(Tin.mass + rf * nd * lenr, (size_t)(rc * nd * lenr), ncclFloat64, p, comm, st));
+            if (rc * nf * lenr) NC(ncclRecv(Tin.pl + rf * nf * lenr, (size_t)(rc * nf * lenr), ncclFloat32, p, comm, st));
+        }
+        NC(ncclGroupEnd());
+    }
+    {
+        const int64_t rf = plan[r].recv_layer_first;
+        if (nl * nd * lenr)
+            CU(cudaMemcpyAsync(Tin.mass + rf * nd * lenr, bm(stage_fwd, r), (size_t)(nl * nd * lenr) * 8,
+                               cudaMemcpyDeviceToDevice, st));
+        if (nl * nf * lenr)
+            CU(cudaMemcpyAsync(Tin.pl + rf * nf * lenr, bf(stage_fwd, r), (size_t)(nl * nf * lenr) * 4,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    // local sweep of whole lines along D-1 on the slab (periodic, no halo)
+    if (T.cells > 0) {
+        Sweep swT = sw;
+        swT.wrap = 1;
+        int64_t n_T = 1;
+        for (int d = 0; d < kMaxDim; ++d) {
+            swT.fstride[d] = 0;
+            if (d < D && (sw.fmask >> d & 1u)) {
+                swT.fstride[d] = n_T;
+                n_T *= T.n[d];
+            }
+        }
+        const double* fT = nullptr;
+        if (dfield) {
+            if (g->tfield_cap < n_T) {
+                CU(cudaStreamSynchronize(st));
+                cudaFree(g->d_tfield);
+                g->d_tfield = nullptr;
+                g->tfield_cap = 0;
+                CU(cudaMalloc(&g->d_tfield, (size_t)std::max<int64_t>(n_T, 1) * sizeof(double)));
+                g->tfield_cap = n_T;
+            }
+            CU(launch_field_slab(dfield, n_T, sw.fmask, T, L, e, plan[r].recv_slab_first, g->d_tfield, st));
+            g->launches += 1;
+            fT = g->d_tfield;
+        }
+        (void)n_entries;
+        CU(launch_weights(T, T.n[D - 1], fT, shift, n_T, g->w, g->d_err, st));
+        g->launches += 1;
+        g->w_const = false;
+        swT.shift = g->w.shift;
+        swT.smod = g->w.smod;
+        swT.copy = g->w.copy;
+        swT.ab = g->w.ab;
+        swT.rec = g->w.rec;
+        sldg_status s2 = run_sweep(g, swT, Tin, Tout, 0, T.layers, &T);
+        if (s2 != SLDG_OK) return s2;
+    }
+    // inverse: exchange back, self copy, unpack into dst
+    if (P > 1) {
+        NC(ncclGroupStart());
+        for (int p = 0; p < P; ++p) {
+            if (p == r) continue;
+            const int64_t rf = plan[p].recv_layer_first, rc = plan[p].recv_layer_count;
+            if (rc * nd * lenr) NC(ncclSend(Tout.mass + rf * nd * lenr, (size_t)(rc * nd * lenr), ncclFloat64, p, comm, st));
+            if (rc * nf * lenr) NC(ncclSend(Tout.pl + rf * nf * lenr, (size_t)(rc * nf * lenr), ncclFloat32, p, comm, st));
+            const int64_t len = plan[p].send_slab_count * Mp;
+            if (nl * nd * len) NC(ncclRecv(bm(stage_inv, p), (size_t)(nl * nd * len), ncclFloat64, p, comm, st));
+            if (nl * nf * len) NC(ncclRecv(bf(stage_inv, p), (size_t)(nl * nf * len), ncclFloat32, p, comm, st));
+        }
+        NC(ncclGroupEnd());
+    }
+    {
+        const int64_t rf = plan[r].recv_layer_first;
+        if (nl * nd * lenr)
+            CU(cudaMemcpyAsync(bm(stage_inv, r), Tout.mass + rf * nd * lenr, (size_t)(nl * nd * lenr) * 8,
+                               cudaMemcpyDeviceToDevice, st));
+        if (nl * nf * lenr)
+            CU(cudaMemcpyAsync(bf(stage_inv, r), Tout.pl + rf * nf * lenr, (size_t)(nl * nf * lenr) * 4,
+                               cudaMemcpyDeviceToDevice, st));
+    }
+    for (int p = 0; p < P; ++p) {
+        CU(launch_tr_block(L, dst, nl, plan[p].send_slab_first * Mp, plan[p].send_slab_count * Mp, bm(stage_inv, p),
+                           bf(stage_inv, p), false, st));
+        g->launches += 1;
+    }
+    g->transposes += 1;
+    return SLDG_OK;
+}
+
 sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field, bool field_on_device,
                         uint32_t mask)
 {
@@ -358,9 +529,14 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
         if (st != SLDG_OK) return st;
     } else {
         int64_t left = std::max<int64_t>(0, imax + 1), right = std::max<int64_t>(0, -imin);
-        if (left > L.pad || right > L.pad)
-            return fail(SLDG_ENOTSUP, "halo of " + std::to_string(std::max(left, right)) +
-                                          " layers exceeds max_halo=" + std::to_string(L.pad));
+        const int P = g->world;
+        if (g->force_transpose || left > L.pad || right > L.pad ||
+            (P > 1 && (left + right) * P > 2 * L.layers * (P - 1))) {
+            st = transpose_sweep(g, sw, dfield, shift, n_entries, src, dst);
+            if (st != SLDG_OK) return st;
+            g->cur = 1 - g->cur;
+            return SLDG_OK;
+        }
         sw.wrap = 0;
         CU(cudaEventRecord(g->ev_ready, g->stream));
         CU(cudaStreamWaitEvent(g->comm_stream, g->ev_ready, 0));
@@ -430,6 +606,27 @@ sldg_status sldg_layer_owner(int64_t n, int world, int64_t layer, int* owner, in
     if (n < 1 || world < 1 || world > n || layer < 0 || layer >= n || !owner)
         return fail(SLDG_EINVAL, "bad arguments");
     *owner = owner_of(n, world, layer, local);
+    return SLDG_OK;
+}
+
+sldg_status sldg_transpose_plan(int64_t n_outer, int64_t n_slab, int world, int rank, int64_t* out)
+{
+    if (n_outer < 1 || n_slab < 1 || world < 1 || world > n_outer || rank < 0 || rank >= world || !out)
+        return fail(SLDG_EINVAL, "bad arguments");
+    const std::vector<TrPart> ps = transpose_plan(n_outer, n_slab, world, rank);
+    for (int p = 0; p < world; ++p) {
+        const TrPart& t = ps[p];
+        const int64_t v[8] = {t.send_layer_first, t.send_layer_count, t.send_slab_first, t.send_slab_count,
+                              t.recv_layer_first, t.recv_layer_count, t.recv_slab_first, t.recv_slab_count};
+        for (int i = 0; i < 8; ++i) out[8 * p + i] = v[i];
+    }
+    return SLDG_OK;
+}
+
+sldg_status sldg_transpose_count(sldg_grid g, int64_t* n)
+{
+    if (!g || !n) return fail(SLDG_EINVAL, "null argument");
+    *n = g->transposes;
     return SLDG_OK;
 }
 
@@ -517,7 +714,8 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
         for (int d = 0; d < D - 1; ++d) L.L *= L.n[d];
         split(L.n[D - 1], world, rank, &L.first_layer, &L.layers);
     }
-    g->halo_mode = (world > 1) || (dist && (dist->flags & SLDG_DIST_FORCE_HALO) && D >= 2);
+    g->halo_mode = (world > 1) || (dist && (dist->flags & (SLDG_DIST_FORCE_HALO | SLDG_DIST_FORCE_TRANSPOSE)) && D >= 2);
+    g->force_transpose = dist && (dist->flags & SLDG_DIST_FORCE_TRANSPOSE) && D >= 2;
     L.pad = g->halo_mode ? ((dist->max_halo > 0) ? dist->max_halo : 2) : 0;
     L.cells = L.layers * L.L;
     g->rank = rank;
@@ -588,6 +786,8 @@ sldg_status sldg_destroy(sldg_grid g)
     cudaFree(g->d_scalar);
     cudaFree(g->d_err);
     cudaFree(g->d_range);
+    cudaFree(g->t_alloc);
+    cudaFree(g->d_tfield);
     cudaFree(g->d_stage);
     if (g->h_stage) cudaFreeHost(g->h_stage);
     for (auto& p : g->ev_pairs) {

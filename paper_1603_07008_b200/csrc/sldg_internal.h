@@ -144,6 +144,11 @@ cudaError_t launch_fill_separable(const Layout& lay, const Arrays& a, int n_term
                                   const double* d_tables, cudaStream_t s);
 cudaError_t launch_field_range(const double* d_field, int64_t n, double shift, int64_t* d_out2,
                                cudaStream_t s);
+// transpose path (sldg_abi.cu transpose_sweep): one (layer range, inner range) message block
+cudaError_t launch_tr_block(const Layout& lay, const Arrays& a, int64_t nl, int64_t first, int64_t len, double* bm,
+                            float* bf, bool pack, cudaStream_t s);
+cudaError_t launch_field_slab(const double* in, int64_t n_out, uint32_t mask, const Layout& nT, const Layout& nF,
+                              int sd, int64_t off, double* out, cudaStream_t s);
 
 constexpr int kMassBlocks = 592;  // 4 x 148 SMs; fixed => deterministic reduction order
 
@@ -178,4 +183,10 @@ struct sldg_grid_s : public sldg::Grid {
     cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
     int64_t* d_range = nullptr;
     bool halo_mode = false;  // sweeps along the layer dim read halo layers (sharded, or forced)
+    bool force_transpose = false;  // every sweep along the layer dim takes the transpose path
+    void* t_alloc = nullptr;       // transpose path: two slab arrays + receive staging
+    size_t t_bytes = 0;
+    double* d_tfield = nullptr;    // transpose path: the field restricted to this rank's slab
+    int64_t tfield_cap = 0;
+    int64_t transposes = 0;        // sweeps that took the transpose path
 };

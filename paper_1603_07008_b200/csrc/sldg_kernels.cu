@@ -4,12 +4,15 @@
 //   mass            a9 deterministic fp64 reduction of the mass slot
 //   set / get       host AoS fp64 <-> device split layout (RNE narrowing)
 //   fills           synthetic inputs (counter-based random, separable Landau)
+//   tr_block        pack / unpack of the transpose path of a sharded sweep
 //
 // Arithmetic is fp64 throughout (reading R6): fp32 slots are promoted exactly on load and
 // rounded to nearest-even on store (__double2float_rn; no fast-math, no FTZ).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+
+#include <algorithm>
 
 #include "sldg_internal.h"
 
@@ -408,6 +411,72 @@ __global__ void field_range_kernel(const double* __restrict__ field, int64_t n, 
 cudaError_t launch_field_range(const double* d_field, int64_t n, double shift, int64_t* d_out2, cudaStream_t s)
 {
     field_range_kernel<<<1, 256, 0, s>>>(d_field, n, shift, d_out2);
+    return cudaGetLastError();
+}
+
+// ---- transpose path of a sweep along the sharded dim (sldg_abi.cu transpose_sweep) ----------
+// Message layout of one (layer range, inner range) block: fp64 part [layer][q < nd][len], then
+// fp32 part [layer][q >= nd][len]; the inner range [first, first + len) of every plane of the
+// padded layers pad .. pad + nl - 1.  pack: array -> block, unpack: block -> array.
+template <bool PACK>
+__global__ void tr_block_kernel(Layout lay, Arrays a, int64_t nl, int64_t first, int64_t len, double* bm,
+                                float* bf)
+{
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t lq = blockIdx.y + (int64_t)gridDim.y * blockIdx.z;  // layer * K + q
+    if (j >= len || lq >= nl * lay.K) return;
+    const int64_t l = lq / lay.K;
+    const int q = (int)(lq - l * lay.K);
+    const int64_t lp = lay.pad + l;
+    if (q < lay.nd) {
+        double* p = dslot(a, lp, lay.nd, q, lay.L, first + j);
+        double* b = bm + (l * lay.nd + q) * len + j;
+        if (PACK) *b = *p;
+        else *p = *b;
+    } else {
+        float* p = fslot(a, lp, lay.K, lay.nd, q, lay.L, first + j);
+        float* b = bf + (l * (lay.K - lay.nd) + (q - lay.nd)) * len + j;
+        if (PACK) *b = *p;
+        else *p = *b;
+    }
+}
+
+cudaError_t launch_tr_block(const Layout& lay, const Arrays& a, int64_t nl, int64_t first, int64_t len, double* bm,
+                            float* bf, bool pack, cudaStream_t s)
+{
+    if (nl <= 0 || len <= 0) return cudaSuccess;
+    const int64_t rows = nl * lay.K;
+    const unsigned gy = (unsigned)std::min<int64_t>(rows, 65535), gz = (unsigned)((rows + gy - 1) / gy);
+    dim3 grid((unsigned)((len + 255) / 256), gy, gz);
+    if (pack) tr_block_kernel<true><<<grid, 256, 0, s>>>(lay, a, nl, first, len, bm, bf);
+    else tr_block_kernel<false><<<grid, 256, 0, s>>>(lay, a, nl, first, len, bm, bf);
+    return cudaGetLastError();
+}
+
+// field entries of a slab grid: out[e'] = in[e] where e' indexes the masked dims with extents
+// nT and e the same cell of the full extents nF, dim `sd` offset by `off`.
+__global__ void field_slab_kernel(const double* in, int64_t n_out, uint32_t mask, Layout nT, Layout nF, int sd,
+                                  int64_t off, double* out)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= n_out) return;
+    int64_t rem = t, e = 0, stride = 1;
+    for (int d = 0; d < nT.D; ++d) {
+        if (!(mask >> d & 1u)) continue;
+        int64_t i = rem % nT.n[d];
+        rem /= nT.n[d];
+        if (d == sd) i += off;
+        e += i * stride;
+        stride *= nF.n[d];
+    }
+    out[t] = in[e];
+}
+
+cudaError_t launch_field_slab(const double* in, int64_t n_out, uint32_t mask, const Layout& nT, const Layout& nF,
+                              int sd, int64_t off, double* out, cudaStream_t s)
+{
+    if (n_out <= 0) return cudaSuccess;
+    field_slab_kernel<<<(unsigned)((n_out + 255) / 256), 256, 0, s>>>(in, n_out, mask, nT, nF, sd, off, out);
     return cudaGetLastError();
 }
 

@@ -27,7 +27,7 @@ EXPORTS = [
     "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
     "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_halo_plan", "sldg_layer_owner",
     "sldg_sweep_kernel", "sldg_vp_create", "sldg_vp_destroy", "sldg_vp_density", "sldg_vp_field",
-    "sldg_vp_step",
+    "sldg_vp_step", "sldg_transpose_plan", "sldg_transpose_count",
 ]
 
 
@@ -50,6 +50,7 @@ class Dist(ctypes.Structure):
                 ("nccl_comm", ctypes.c_void_p), ("max_halo", ctypes.c_int), ("flags", ctypes.c_int)]
 
 SLDG_DIST_FORCE_HALO = 1
+SLDG_DIST_FORCE_TRANSPOSE = 2
 
 
 _lib = None
@@ -88,6 +89,8 @@ def lib():
         "sldg_halo_widths": [i64, i64, i64p, i64p],
         "sldg_halo_plan": [i64, ctypes.c_int, ctypes.c_int, i64, i64, i64, i64p, i64, i64p],
         "sldg_layer_owner": [i64, ctypes.c_int, i64, ctypes.POINTER(ctypes.c_int), i64p],
+        "sldg_transpose_plan": [i64, i64, ctypes.c_int, ctypes.c_int, i64p],
+        "sldg_transpose_count": [vp, i64p],
         "sldg_vp_create": [vp, ctypes.c_int, ctypes.POINTER(vp)],
         "sldg_vp_destroy": [vp],
         "sldg_vp_density": [vp, dp],
@@ -140,6 +143,14 @@ def halo_plan(n: int, world: int, rank: int, pad: int, left: int, right: int):
     return [tuple(buf[4 * i:4 * i + 4]) for i in range(cnt.value)]
 
 
+def transpose_plan(n_outer: int, n_slab: int, world: int, rank: int):
+    """[(send_layer_first, send_layer_count, send_slab_first, send_slab_count, recv_layer_first,
+    recv_layer_count, recv_slab_first, recv_slab_count)] per peer -- the transpose path's plan."""
+    buf = (ctypes.c_int64 * (8 * world))()
+    _check(lib().sldg_transpose_plan(n_outer, n_slab, world, rank, buf))
+    return [tuple(buf[8 * p:8 * p + 8]) for p in range(world)]
+
+
 def layer_owner(n: int, world: int, layer: int):
     o, loc = ctypes.c_int(), ctypes.c_int64()
     _check(lib().sldg_layer_owner(n, world, layer, ctypes.byref(o), ctypes.byref(loc)))
@@ -151,7 +162,7 @@ class Grid:
 
     def __init__(self, cells, k: int, lo=None, hi=None, precision: str = "mixed",
                  rank: int = 0, world: int = 1, unique_id: bytes | None = None, max_halo: int = 0,
-                 force_halo: bool = False):
+                 force_halo: bool = False, force_transpose: bool = False):
         cells = [int(c) for c in cells]
         self.D = len(cells)
         self.cells = cells
@@ -171,12 +182,13 @@ class Grid:
             prec = {"mixed": SLDG_MIXED, "fp64": SLDG_FP64}[precision]
         dist_p = None
         self._uid = None
-        if world > 1 or force_halo:
+        if world > 1 or force_halo or force_transpose:
             uid = None
             if world > 1:
                 self._uid = ctypes.create_string_buffer(unique_id, 128)
                 uid = ctypes.cast(self._uid, ctypes.c_void_p)
-            self._dist = Dist(rank, world, uid, None, max_halo, SLDG_DIST_FORCE_HALO if force_halo else 0)
+            flags = (SLDG_DIST_FORCE_HALO if force_halo else 0) | (SLDG_DIST_FORCE_TRANSPOSE if force_transpose else 0)
+            self._dist = Dist(rank, world, uid, None, max_halo, flags)
             dist_p = ctypes.byref(self._dist)
         h = ctypes.c_void_p()
         if n_double is None:
@@ -270,6 +282,11 @@ class Grid:
 
     def launch_count(self) -> int:
         return int(lib().sldg_launch_count(self.h))
+
+    def transpose_count(self) -> int:
+        n = ctypes.c_int64()
+        _check(lib().sldg_transpose_count(self.h, ctypes.byref(n)))
+        return n.value
 
     def sweep_kernel(self, dim: int) -> str:
         return lib().sldg_sweep_kernel(self.h, int(dim)).decode()

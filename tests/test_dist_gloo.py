@@ -166,3 +166,104 @@ def test_sharded_sweep_from_halos_matches_global_oracle(world):
     for p in procs:
         p.join(timeout=60)
     assert all(r[1] == "ok" for r in res), res
+
+
+# ------------------------------------------------------------------------------ transpose path
+def _transpose_worker(rank, world, port, cases, q):
+    """The transpose path of a sweep along the sharded dim, run with gloo on CPU
+    exactly as `sldg_transpose_plan` lays it out: rank r sends p its layers restricted to p's
+    slab of dim D-2, receives whole lines for its own slab, sweeps them (oracle, periodic), and
+    the inverse exchange returns them.  The result must equal the global oracle sweep."""
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    import sldg_inputs
+    from paper_1603_07008_b200 import sldg
+    try:
+        for dims, k, shift, use_field in cases:
+            n0, ns, no = dims
+            K = k ** 3
+            c = oracle.round_layout(sldg_inputs.random_coeffs(dims, k, 7008), K, 1)
+            glob = c.reshape(no, ns, n0, K)
+            field = np.linspace(-3.3 * no, 2.1 * no, n0 * ns) if use_field else None
+            mask = 0b011 if use_field else 0
+            want = oracle.advect(c, dims, k, 2, shift=shift, field=field, field_mask=mask,
+                                 n_double=1).reshape(no, ns, n0, K)
+            plan = sldg.transpose_plan(no, ns, world, rank)
+            f_r, c_r = plan[rank][0], plan[rank][1]
+            a_r, s_r = plan[rank][6], plan[rank][7]
+            mine = torch.from_numpy(glob[f_r:f_r + c_r].copy())
+            T = torch.full((no, s_r, n0, K), float("nan"), dtype=torch.float64)
+            reqs = []
+            for p in range(world):
+                sf, sc, af, ac, rf, rc, _, _ = plan[p]
+                blk = mine[:, af:af + ac].contiguous()
+                if p == rank:
+                    T[rf:rf + rc] = blk
+                    continue
+                reqs.append(dist.isend(blk, dst=p))
+                buf = torch.empty((rc, s_r, n0, K), dtype=torch.float64)
+                reqs.append((rf, rc, buf, dist.irecv(buf, src=p)))
+            for r_ in reqs:
+                if isinstance(r_, tuple):
+                    rf, rc, buf, h = r_
+                    h.wait()
+                    T[rf:rf + rc] = buf
+                else:
+                    r_.wait()
+            assert not torch.isnan(T).any()
+            # local sweep of whole lines on the slab; the field restricted to the slab (dim 1 offset a_r)
+            tf = None
+            if use_field:
+                tf = field.reshape(ns, n0)[a_r:a_r + s_r].reshape(-1)
+            if s_r > 0:  # a rank can own no slab when n_slab < world
+                Tout = oracle.advect(T.numpy().reshape(-1, K), [n0, s_r, no], k, 2, shift=shift, field=tf,
+                                     field_mask=mask, n_double=1).reshape(no, s_r, n0, K)
+                Tout = torch.from_numpy(Tout)
+            else:
+                Tout = T
+            out = torch.full_like(mine, float("nan"))
+            reqs = []
+            for p in range(world):
+                sf, sc, af, ac, rf, rc, _, _ = plan[p]
+                if p == rank:
+                    out[:, af:af + ac] = Tout[rf:rf + rc]
+                    continue
+                reqs.append(dist.isend(Tout[rf:rf + rc].contiguous(), dst=p))
+                buf = torch.empty((c_r, ac, n0, K), dtype=torch.float64)
+                reqs.append((af, ac, buf, dist.irecv(buf, src=p)))
+            for r_ in reqs:
+                if isinstance(r_, tuple):
+                    af, ac, buf, h = r_
+                    h.wait()
+                    out[:, af:af + ac] = buf
+                else:
+                    r_.wait()
+            assert np.array_equal(out.numpy(), want[f_r:f_r + c_r]), (rank, dims, shift)
+            dist.barrier()
+        q.put((rank, "ok"))
+    except Exception:  # pragma: no cover
+        import traceback
+        q.put((rank, traceback.format_exc()))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_transpose_path_matches_global_oracle(world):
+    import __graft_entry__
+    __graft_entry__.build()
+    # (dims [n0, n_slab, n_outer], k, constant shift, per-line field over dims 0 and 1)
+    cases = [([4, 5, 7], 2, 5.3, False), ([3, 6, 8], 2, -9.75, True), ([2, 2, 9], 1, 0.5, False)]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_transpose_worker, args=(r, world, port, cases, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] == "ok" for r in res), res

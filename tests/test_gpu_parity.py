@@ -405,6 +405,42 @@ def test_forced_halo_path_matches_oracle(dims, k, precision):
         ref = oracle.advect(ref_in, dims, k, d, shift=shift, field=field, field_mask=mask,
                             n_double=n_double(precision, K))
         assert_parity(g.get_coeffs(), ref, K, precision, f"halo dims={dims} dim={d} nu={shift}", ref_in, d, k)
-    with pytest.raises(SldgError):  # halo of 5 layers > max_halo = 3
-        g.advect(D - 1, shift=4.5)
+    # a halo of 5 layers > max_halo = 3 takes the transpose path
+    assert g.transpose_count() == 0
+    g.set_coeffs(c)
+    g.advect(D - 1, shift=4.5)
+    assert g.transpose_count() == 1
+    ref = oracle.advect(ref_in, dims, k, D - 1, shift=4.5, n_double=n_double(precision, K))
+    assert_parity(g.get_coeffs(), ref, K, precision, f"auto-transpose dims={dims}", ref_in, D - 1, k)
+    g.destroy()
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+@pytest.mark.parametrize("dims,k", [([64, 24], 3), ([32, 6, 20], 2), ([8, 5, 3, 11], 3), ([12, 4, 7], 4)])
+def test_forced_transpose_path_matches_oracle(dims, k, precision):
+    """The transpose path (pack per slab, all-to-all, whole-line local sweep with the field
+    restricted to the slab, inverse exchange, unpack) on one GPU (SLDG_DIST_FORCE_TRANSPOSE):
+    sweeps along the layer dim with small and large constant shifts and per-line fields over
+    the slab dim and another dim; sweeps along the other dims stay on the local path."""
+    D, K = len(dims), k ** len(dims)
+    c = sldg_inputs.random_coeffs(dims, k, 99)
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision, force_transpose=True, max_halo=1)
+    rng = np.random.default_rng(D * 10 + k)
+    nf = dims[0] * dims[D - 2] if D > 2 else dims[0]
+    fmask = (1 | (1 << (D - 2))) if D > 2 else 1
+    cases = [(D - 1, 1.37, None, 0), (D - 1, -7.75 - dims[-1], None, 0), (D - 1, 3.0, None, 0),
+             (D - 1, 0.0, rng.uniform(-2.5 * dims[-1], 2.5 * dims[-1], nf), fmask), (0, 2.6, None, 0)]
+    n_tr = 0
+    for d, shift, field, mask in cases:
+        g.set_coeffs(c)
+        g.advect(d, shift=shift, field=field, field_mask=mask)
+        n_tr += (d == D - 1)
+        assert g.transpose_count() == n_tr
+        ref = oracle.advect(ref_in, dims, k, d, shift=shift, field=field, field_mask=mask,
+                            n_double=n_double(precision, K))
+        got = g.get_coeffs()
+        if shift == 3.0:
+            assert got.tobytes() == ref.tobytes()  # integer shift: exact rotation through the transpose
+        assert_parity(got, ref, K, precision, f"transpose dims={dims} dim={d} nu={shift}", ref_in, d, k)
     g.destroy()
