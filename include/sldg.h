@@ -136,6 +136,19 @@ sldg_status sldg_advect(sldg_grid g, int dim, double shift, const double* field,
 sldg_status sldg_advect_device(sldg_grid g, int dim, double shift, const double* d_field,
                                uint32_t field_mask);
 
+/* Gauss-node velocity treatment of an x-sweep (NEXT-3, reading V7): a sweep along
+ * `dim` whose CFL number varies with the velocity coordinate of dim `vdim` INSIDE each v-cell.
+ * Per v-cell j: modal -> nodal in vdim at the k Gauss-Legendre nodes, one SLDG line
+ * update per node with its own CFL number, nodal -> modal by Gauss quadrature
+ * (S:303).  nodal_nu[j * k + n] = nu at node n (ascending xi_n) of v-cell j (GLOBAL j),
+ * HOST memory (sldg_advect_vnodes) or DEVICE memory (_device; non-finite entries leave their
+ * v-cell unchanged and make the next blocking call return EINVAL).  fp64 arithmetic, RNE
+ * stores; no exact-copy path (the nodal transform pair is the identity only up to rounding).
+ * Errors: EINVAL (dims equal / out of range, null or non-finite field), ENOTSUP (k > 4; dim
+ * is the sharded layer dim); the nodes of one v-cell spanning more than 5 integer parts make
+ * that cell's lines unchanged with the sticky EINVAL).  Asynchronous. */
+sldg_status sldg_advect_vnodes(sldg_grid g, int dim, int vdim, const double* nodal_nu);
+sldg_status sldg_advect_vnodes_device(sldg_grid g, int dim, int vdim, const double* d_nodal_nu);
 /* Total mass M = (prod_d h_d) * sum_cells c_{cell,0}, a deterministic
  * fixed-order fp64 reduction; collective over ranks (rank-ordered sum).  Blocks. */
 sldg_status sldg_mass(sldg_grid g, double* mass_out);
@@ -240,6 +253,10 @@ sldg_status sldg_vp_density(sldg_vp vp, double* rho_out);
  * f -- into the optional HOST outputs: e_out (dx * N_x centre values), e_coef (dx = 1 only:
  * N_x * (k+1) Legendre coefficients of E per cell), energy.  Blocks when any output is given. */
 sldg_status sldg_vp_field(sldg_vp vp, const double* rho, double* e_out, double* e_coef, double* energy);
+/* on != 0: the x sweeps of sldg_vp_step use the Gauss-node velocity treatment (V7,
+ * sldg_advect_vnodes: nu at the k Gauss nodes of every v-cell) instead of the cell-centre
+ * velocity (V5).  ENOTSUP for k > 4. */
+sldg_status sldg_vp_set_nodal(sldg_vp vp, int on);
 /* One Strang step of length dt (V6).  energy_out (HOST or NULL): electric energy of the
  * mid-step field (blocks when given).  Asynchronous otherwise. */
 sldg_status sldg_vp_step(sldg_vp vp, double dt, double* energy_out);

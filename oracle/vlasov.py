@@ -146,19 +146,29 @@ def x_field(dims, dx: int, lo, hi, c: int, tau: float) -> np.ndarray:
     return v * tau / hx
 
 
-def strang_step(c: np.ndarray, dims, k: int, dx: int, lo, hi, dt: float, n_double: int):
+def _x_sweep(c, dims, k, dx, lo, hi, a, tau, n_double, nodal):
+    if not nodal:  # V5: cell-centre velocity
+        return _advect(c, dims, k, a, field=x_field(dims, dx, lo, hi, a, tau), field_mask=1 << (dx + a),
+                       n_double=n_double)
+    # V7 (NEXT-3): one CFL number per Gauss node of every v_a cell
+    from . import vnodes
+    nv = int(dims[dx + a])
+    nu = vnodes.nodal_velocity_field(nv, lo[dx + a], hi[dx + a], k, tau / ((hi[a] - lo[a]) / dims[a]))
+    return vnodes.advect_vnodes(c, dims, k, a, dx + a, nu, n_double=n_double)
+
+
+def strang_step(c: np.ndarray, dims, k: int, dx: int, lo, hi, dt: float, n_double: int, nodal: bool = False):
     """V6: one Strang step; returns (new coefficients, [E_c at centres], energy)
-    with the field of the mid-step density."""
+    with the field of the mid-step density.  nodal=True: x-sweeps by the Gauss-node velocity
+    treatment (V7) instead of the cell-centre reading (V5)."""
     dims = [int(n) for n in dims]
     for a in range(dx):  # x half-steps
-        c = _advect(c, dims, k, a, field=x_field(dims, dx, lo, hi, a, dt / 2),
-                    field_mask=1 << (dx + a), n_double=n_double)
+        c = _x_sweep(c, dims, k, dx, lo, hi, a, dt / 2, n_double, nodal)
     es, w = field(c, dims, k, dx, lo, hi)
     xmask = (1 << dx) - 1
     for a in range(dx):  # v full steps, nu = E_a(x centre) dt / h_va
         hv = (hi[dx + a] - lo[dx + a]) / dims[dx + a]
         c = _advect(c, dims, k, dx + a, field=es[a] * dt / hv, field_mask=xmask, n_double=n_double)
     for a in range(dx):
-        c = _advect(c, dims, k, a, field=x_field(dims, dx, lo, hi, a, dt / 2),
-                    field_mask=1 << (dx + a), n_double=n_double)
+        c = _x_sweep(c, dims, k, dx, lo, hi, a, dt / 2, n_double, nodal)
     return c, es, w

@@ -557,6 +557,54 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
     return SLDG_OK;
 }
 
+sldg_status advect_vnodes_impl(sldg_grid g, int dim, int vdim, const double* nodal, bool on_device)
+{
+    const Layout& L = g->lay;
+    if (dim < 0 || dim >= L.D || vdim < 0 || vdim >= L.D || dim == vdim)
+        return fail(SLDG_EINVAL, "dim and vdim must be distinct dims of the grid");
+    if (!nodal) return fail(SLDG_EINVAL, "null nodal field");
+    if (L.k > 4) return fail(SLDG_ENOTSUP, "the Gauss-node sweep supports k <= 4");
+    if (g->halo_mode && dim == L.D - 1) return fail(SLDG_ENOTSUP, "Gauss-node sweep along the sharded dim");
+    const int64_t nv = L.n[vdim], n_entries = nv * L.k;
+    const double* dn = nodal;
+    if (!on_device) {
+        for (int64_t i = 0; i < n_entries; ++i)
+            if (!(fabs(nodal[i]) < 4.611686018427387904e18))
+                return fail(SLDG_EINVAL, "non-finite or |nu| >= 2^62 entry in the nodal field");
+        sldg_status st = ensure_field(g, n_entries);
+        if (st != SLDG_OK) return st;
+        CU(cudaMemcpyAsync(g->d_field, nodal, n_entries * sizeof(double), cudaMemcpyHostToDevice, g->stream));
+        dn = g->d_field;
+    }
+    const int64_t words = vnode_rec_words(L.k) * nv;
+    if (g->vnrec_cap < words) {
+        CU(cudaStreamSynchronize(g->stream));
+        cudaFree(g->d_vnrec);
+        g->d_vnrec = nullptr;
+        g->vnrec_cap = 0;
+        CU(cudaMalloc(&g->d_vnrec, words * sizeof(double)));
+        g->vnrec_cap = words;
+    }
+    CU(launch_vnode_weights(L.k, dn, nv, g->d_vnrec, g->d_err, g->stream));
+    g->launches += 1;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (g->profile) {
+        e0 = pool_event(g);
+        e1 = pool_event(g);
+        CU(cudaEventRecord(e0, g->stream));
+    }
+    CU(launch_vnode_sweep(L, dim, vdim, g->d_vnrec, g->buf[g->cur], g->buf[1 - g->cur], g->stream));
+    g->launches += 1;
+    if (g->profile) {
+        CU(cudaEventRecord(e1, g->stream));
+        g->ev_pairs.push_back({e0, e1});
+        g->ev_bytes.push_back(2.0 * (double)bytes_per_cell(L) * (double)L.cells);
+        g->ev_dim.push_back(dim);
+    }
+    g->cur = 1 - g->cur;
+    return SLDG_OK;
+}
+
 }  // namespace
 
 sldg_status sldg::set_error(sldg_status st, const std::string& msg) { return fail(st, msg); }
@@ -621,6 +669,18 @@ sldg_status sldg_transpose_plan(int64_t n_outer, int64_t n_slab, int world, int 
         for (int i = 0; i < 8; ++i) out[8 * p + i] = v[i];
     }
     return SLDG_OK;
+}
+
+sldg_status sldg_advect_vnodes(sldg_grid g, int dim, int vdim, const double* nodal_nu)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    return advect_vnodes_impl(g, dim, vdim, nodal_nu, false);
+}
+
+sldg_status sldg_advect_vnodes_device(sldg_grid g, int dim, int vdim, const double* d_nodal_nu)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    return advect_vnodes_impl(g, dim, vdim, d_nodal_nu, true);
 }
 
 sldg_status sldg_transpose_count(sldg_grid g, int64_t* n)
@@ -788,6 +848,7 @@ sldg_status sldg_destroy(sldg_grid g)
     cudaFree(g->d_range);
     cudaFree(g->t_alloc);
     cudaFree(g->d_tfield);
+    cudaFree(g->d_vnrec);
     cudaFree(g->d_stage);
     if (g->h_stage) cudaFreeHost(g->h_stage);
     for (auto& p : g->ev_pairs) {

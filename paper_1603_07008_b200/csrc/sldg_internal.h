@@ -144,6 +144,12 @@ cudaError_t launch_fill_separable(const Layout& lay, const Arrays& a, int n_term
                                   const double* d_tables, cudaStream_t s);
 cudaError_t launch_field_range(const double* d_field, int64_t n, double shift, int64_t* d_out2,
                                cudaStream_t s);
+// Gauss-node velocity sweep (sldg_vnodes.cu, NEXT-3)
+constexpr int kVnMaxOfs = 6;  // source offsets per v-cell (nodes' integer parts may differ)
+int64_t vnode_rec_words(int k);
+cudaError_t launch_vnode_weights(int k, const double* d_nodal, int64_t nv, double* d_rec, int* d_err, cudaStream_t s);
+cudaError_t launch_vnode_sweep(const Layout& lay, int d, int e, const double* d_rec, const Arrays& src,
+                               const Arrays& dst, cudaStream_t s);
 // transpose path (sldg_abi.cu transpose_sweep): one (layer range, inner range) message block
 cudaError_t launch_tr_block(const Layout& lay, const Arrays& a, int64_t nl, int64_t first, int64_t len, double* bm,
                             float* bf, bool pack, cudaStream_t s);
@@ -189,4 +195,6 @@ struct sldg_grid_s : public sldg::Grid {
     double* d_tfield = nullptr;    // transpose path: the field restricted to this rank's slab
     int64_t tfield_cap = 0;
     int64_t transposes = 0;        // sweeps that took the transpose path
+    double* d_vnrec = nullptr;     // Gauss-node sweep: per-v-cell operator records
+    int64_t vnrec_cap = 0;
 };

@@ -25,6 +25,7 @@
 #include <string>
 #include <vector>
 
+#include "sldg_basis.cuh"
 #include "sldg_internal.h"
 
 using namespace sldg;
@@ -309,6 +310,19 @@ __global__ void vp_x_field_kernel(int64_t nv, double lo_v, double h_v, double ta
     if (i < nv) nu[i] = (lo_v + ((double)i + 0.5) * h_v) * tau / h_x;
 }
 
+// V7 (NEXT-3): nu[i * k + n] = (lo_v + (i + 1/2) h_v + xi_n h_v / 2) * tau / h_x at the Gauss nodes
+__global__ void vp_x_nodal_field_kernel(int64_t nv, int k, double lo_v, double h_v, double tau, double h_x,
+                                        double* nu)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= nv * k) return;
+    double xg[kMaxK], wg[kMaxK];
+    dev_gauss(k, xg, wg);
+    const int64_t i = t / k;
+    const int n = (int)(t - i * k);
+    nu[t] = (lo_v + ((double)i + 0.5) * h_v + xg[n] * h_v / 2) * tau / h_x;
+}
+
 // V5: nu[i_x] = E_c(i_x) * tau / h_v
 __global__ void vp_v_field_kernel(const double* ec, int64_t N, double tau, double h_v, double* nu)
 {
@@ -323,6 +337,7 @@ unsigned nblk(int64_t n, int bs = 256) { return (unsigned)((n + bs - 1) / bs); }
 struct sldg_vp_s {
     sldg_grid g = nullptr;
     int dx = 1, k = 1, Kx = 1;
+    bool nodal = false;        // x sweeps by the Gauss-node velocity treatment (V7)
     int64_t nx[2] = {1, 1}, Nx = 1;
     double hv = 1.0;           // prod_c h_vc
     double* d_partial = nullptr;   // [world][kVSplit][Kx][Nx]
@@ -408,10 +423,19 @@ sldg_status vp_x_sweeps(sldg_vp vp, double tau)
     for (int c = 0; c < vp->dx; ++c) {
         const int dv = vp->dx + c;
         const int64_t nv = g->lay.n[dv];
-        vp_x_field_kernel<<<nblk(nv), 256, 0, g->stream>>>(nv, g->lo[dv], g->h[dv], tau, g->h[c], vp->d_nux[c]);
-        VCU(cudaGetLastError());
-        g->launches += 1;
-        sldg_status st = sldg_advect_device(g, c, 0.0, vp->d_nux[c], 1u << dv);
+        sldg_status st;
+        if (vp->nodal) {
+            vp_x_nodal_field_kernel<<<nblk(nv * vp->k), 256, 0, g->stream>>>(nv, vp->k, g->lo[dv], g->h[dv], tau,
+                                                                             g->h[c], vp->d_nux[c]);
+            VCU(cudaGetLastError());
+            g->launches += 1;
+            st = sldg_advect_vnodes_device(g, c, dv, vp->d_nux[c]);
+        } else {
+            vp_x_field_kernel<<<nblk(nv), 256, 0, g->stream>>>(nv, g->lo[dv], g->h[dv], tau, g->h[c], vp->d_nux[c]);
+            VCU(cudaGetLastError());
+            g->launches += 1;
+            st = sldg_advect_device(g, c, 0.0, vp->d_nux[c], 1u << dv);
+        }
         if (st != SLDG_OK) return st;
     }
     return SLDG_OK;
@@ -462,7 +486,7 @@ sldg_status sldg_vp_create(sldg_grid g, int dx, sldg_vp* out)
     if (dx == 2)
         for (int i = 0; i < 4; ++i) A((void**)&vp->d_c[i], (size_t)vp->Nx * sizeof(double2));
     for (int c = 0; c < dx; ++c) {
-        A((void**)&vp->d_nux[c], (size_t)L.n[dx + c] * sizeof(double));
+        A((void**)&vp->d_nux[c], (size_t)L.n[dx + c] * L.k * sizeof(double));
         A((void**)&vp->d_nuv[c], (size_t)vp->Nx * sizeof(double));
     }
     if (st != SLDG_OK) {
@@ -479,6 +503,14 @@ sldg_status sldg_vp_destroy(sldg_vp vp)
     if (vp->g) cudaStreamSynchronize(vp->g->stream);
     for (void* p : vp->allocs) cudaFree(p);
     delete vp;
+    return SLDG_OK;
+}
+
+sldg_status sldg_vp_set_nodal(sldg_vp vp, int on)
+{
+    if (!vp) return set_error(SLDG_EINVAL, "null handle");
+    if (on && vp->k > 4) return set_error(SLDG_ENOTSUP, "the Gauss-node sweep supports k <= 4");
+    vp->nodal = (on != 0);
     return SLDG_OK;
 }
 

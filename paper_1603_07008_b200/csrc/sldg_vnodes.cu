@@ -1,0 +1,224 @@
+// sldg_vnodes.cu -- Gauss-node velocity treatment of x-sweeps (NEXT-3 of SURVEY 8(f); DESIGN.md
+// 6d, reading V7; oracle/vnodes.py).
+//
+// An x-sweep along dim d whose CFL number varies with the velocity inside a v-cell of dim e:
+// modal -> nodal in e at the k Gauss nodes (P:221-227 nodal basis), one SLDG line update per
+// node with its own nu, nodal -> modal by Gauss quadrature.  All three
+// steps are linear, so per v-cell j they fold into one operator per source offset o:
+//   c'_{(m_e, m_d)}(i) = sum_o sum_{(l_e, l_d)} M_o[m_e m_d][l_e l_d] c_{(l_e, l_d)}(i - o)
+//   M_o = sum_n Tinv[m_e][n] T[n][l_e] (A_n[m_d][l_d] [o == i*_n + 1] + B_n[m_d][l_d] [o == i*_n])
+// with T[n][l] = P_l(xi_n), Tinv[m][n] = w_n (2m+1)/2 P_m(xi_n), (i*_n, A_n, B_n) the plain
+// sweep's decomposition and shift matrices of node n.  Offsets span [min i*_n, max i*_n + 1]
+// (2 cells when every node has the same integer part, 3 when the nodes straddle an integer).
+//   vnode_weights_kernel   one CTA per v-cell: nodes, A_n/B_n, the M_o
+//   vnode_sweep_kernel     one thread per target cell; for every coupled (m_e, m_d) block it
+//                          loads the k^2 coefficients of each source cell and applies the M_o
+// fp64 arithmetic, fp32 slots rounded to nearest-even on store (R6).  There is no exact-copy
+// path: the modal -> nodal -> modal pair is the identity only up to rounding.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "sldg_basis.cuh"
+#include "sldg_internal.h"
+
+namespace sldg {
+
+namespace {
+
+// record of one v-cell: [omin (int64 bits), nofs (int64 bits), M[kVnMaxOfs][k^4]]
+__host__ __device__ __forceinline__ int64_t vn_rec_words(int k) { return 2 + (int64_t)kVnMaxOfs * k * k * k * k; }
+
+__global__ void vnode_weights_kernel(int k, const double* __restrict__ nodal, int64_t nv, double* __restrict__ rec,
+                                     int* __restrict__ err)
+{
+    const int64_t j = blockIdx.x;
+    if (j >= nv) return;
+    __shared__ double sT[kMaxK * kMaxK], sTi[kMaxK * kMaxK];
+    __shared__ double sA[kMaxK * kMaxK * kMaxK], sB[kMaxK * kMaxK * kMaxK];  // [n][m][l]
+    __shared__ int64_t sI[kMaxK];
+    __shared__ int64_t s_omin;
+    __shared__ int s_nofs, s_bad;
+    double* r = rec + j * vn_rec_words(k);
+    if (threadIdx.x == 0) {
+        double xg[kMaxK], wg[kMaxK], P[kMaxK + 2];
+        dev_gauss(k, xg, wg);
+        for (int n = 0; n < k; ++n) {
+            dev_legendre(k - 1, xg[n], P);
+            for (int m = 0; m < k; ++m) {
+                sT[n * k + m] = P[m];
+                sTi[m * k + n] = wg[n] * (0.5 * (2 * m + 1)) * P[m];
+            }
+        }
+        int bad = 0;
+        int64_t omin = INT64_MAX, omax = INT64_MIN;
+        for (int n = 0; n < k; ++n) {
+            const double nu = nodal[j * k + n];
+            double* A = sA + n * k * k;
+            double* B = sB + n * k * k;
+            for (int q = 0; q < k * k; ++q) {
+                A[q] = 0.0;
+                B[q] = ((q / k) == (q % k)) ? 1.0 : 0.0;
+            }
+            int64_t is = 0;
+            if (!(fabs(nu) < 4.611686018427387904e18)) {
+                bad = 1;
+            } else {
+                const double fl = floor(nu);
+                double a = nu - fl;
+                is = (int64_t)fl;
+                if (a >= 1.0) {  // reading R2 edge case
+                    is += 1;
+                    a = 0.0;
+                }
+                if (a != 0.0) build_ab(k, a, A, B);
+            }
+            sI[n] = is;
+            omin = is < omin ? is : omin;
+            omax = (is + 1) > omax ? (is + 1) : omax;
+        }
+        if (bad || omax - omin + 1 > kVnMaxOfs) {
+            bad = 1;
+            omin = 0;
+            omax = 0;  // leave the lines unchanged: identity at offset 0
+        }
+        s_bad = bad;
+        s_omin = omin;
+        s_nofs = (int)(omax - omin + 1);
+        if (bad) atomicExch(err, 1);
+        r[0] = __longlong_as_double((long long)omin);
+        r[1] = __longlong_as_double((long long)(omax - omin + 1));
+    }
+    __syncthreads();
+    const int k2 = k * k, k4 = k2 * k2;
+    double* M = r + 2;
+    for (int t = threadIdx.x; t < kVnMaxOfs * k4; t += blockDim.x) {
+        const int o = t / k4, rem = t % k4;
+        const int me = rem / (k * k2), md = (rem / k2) % k, le = (rem / k) % k, ld = rem % k;
+        double v = 0.0;
+        if (s_bad) {
+            v = (o == 0 && me == le && md == ld) ? 1.0 : 0.0;
+        } else if (o < s_nofs) {
+            const int64_t off = s_omin + o;
+            for (int n = 0; n < k; ++n) {
+                double ab = 0.0;
+                if (off == sI[n] + 1) ab += sA[(n * k + md) * k + ld];
+                if (off == sI[n]) ab += sB[(n * k + md) * k + ld];
+                v = fma(sTi[me * k + n] * sT[n * k + le], ab, v);
+            }
+        }
+        M[t] = v;
+    }
+}
+
+__device__ __forceinline__ double vn_load(const Layout& L, const Arrays& a, int q, int64_t lp, int64_t inner)
+{
+    if (q < L.nd) return *dslot(a, lp, L.nd, q, L.L, inner);
+    return (double)*fslot(a, lp, L.K, L.nd, q, L.L, inner);
+}
+__device__ __forceinline__ void vn_store(const Layout& L, const Arrays& a, int q, int64_t lp, int64_t inner, double v)
+{
+    if (q < L.nd) *dslot(a, lp, L.nd, q, L.L, inner) = v;
+    else *fslot(a, lp, L.K, L.nd, q, L.L, inner) = __double2float_rn(v);
+}
+
+template <int KK>
+__global__ void __launch_bounds__(256) vnode_sweep_kernel(Layout lay, int d, int e, const double* __restrict__ rec,
+                                                         Arrays src, Arrays dst)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= lay.cells) return;
+    const int D = lay.D;
+    const int64_t layer = t / lay.L, inner = t - layer * lay.L;
+    const int64_t lp = lay.pad + layer;
+    // index along d and along e (global)
+    auto idx_of = [&](int dd) -> int64_t {
+        if (dd == D - 1) return lay.first_layer + layer;
+        return (inner / lay.S[dd]) % lay.n[dd];
+    };
+    const int64_t id = idx_of(d), j = idx_of(e);
+    const double* r = rec + j * vn_rec_words(KK);
+    const int64_t omin = (int64_t)__double_as_longlong(__ldg(&r[0]));
+    const int nofs = (int)__double_as_longlong(__ldg(&r[1]));
+    const double* M = r + 2;
+    constexpr int K2 = KK * KK, K4 = K2 * K2;
+    // source positions per offset
+    int64_t s_lp[kVnMaxOfs], s_in[kVnMaxOfs];
+    const int64_t nd = lay.n[d];
+#pragma unroll
+    for (int o = 0; o < kVnMaxOfs; ++o) {
+        int64_t sidx = (id - (omin + o)) % nd;
+        if (sidx < 0) sidx += nd;
+        if (d == D - 1) {
+            s_lp[o] = lay.pad + (sidx - lay.first_layer);
+            s_in[o] = inner;
+        } else {
+            s_lp[o] = lp;
+            s_in[o] = inner + (sidx - id) * lay.S[d];
+        }
+    }
+    int kd = 1, ke = 1;
+    for (int x = 0; x < d; ++x) kd *= KK;
+    for (int x = 0; x < e; ++x) ke *= KK;
+    const int nblk = lay.K / K2;
+    for (int b = 0; b < nblk; ++b) {
+        // slot base of block b: the other dims' indices (all but d, e) from b
+        int q0 = 0, bb = b, kp = 1;
+        for (int x = 0; x < D; ++x) {
+            if (x != d && x != e) {
+                q0 += (bb % KK) * kp;
+                bb /= KK;
+            }
+            kp *= KK;
+        }
+        double out[K2];
+#pragma unroll
+        for (int m = 0; m < K2; ++m) out[m] = 0.0;
+        for (int o = 0; o < nofs; ++o) {
+            double v[K2];
+#pragma unroll
+            for (int le = 0; le < KK; ++le)
+#pragma unroll
+                for (int ld = 0; ld < KK; ++ld) v[le * KK + ld] = vn_load(lay, src, q0 + ld * kd + le * ke, s_lp[o], s_in[o]);
+            const double* Mo = M + o * K4;
+#pragma unroll
+            for (int m = 0; m < K2; ++m) {
+                double acc = out[m];
+#pragma unroll
+                for (int l = 0; l < K2; ++l) acc = fma(__ldg(&Mo[m * K2 + l]), v[l], acc);
+                out[m] = acc;
+            }
+        }
+#pragma unroll
+        for (int me = 0; me < KK; ++me)
+#pragma unroll
+            for (int md = 0; md < KK; ++md) vn_store(lay, dst, q0 + md * kd + me * ke, lp, inner, out[me * KK + md]);
+    }
+}
+
+}  // namespace
+
+int64_t vnode_rec_words(int k) { return vn_rec_words(k); }
+
+cudaError_t launch_vnode_weights(int k, const double* d_nodal, int64_t nv, double* d_rec, int* d_err, cudaStream_t s)
+{
+    vnode_weights_kernel<<<(unsigned)nv, 128, 0, s>>>(k, d_nodal, nv, d_rec, d_err);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vnode_sweep(const Layout& lay, int d, int e, const double* d_rec, const Arrays& src,
+                               const Arrays& dst, cudaStream_t s)
+{
+    const unsigned blocks = (unsigned)((lay.cells + 255) / 256);
+    if (blocks == 0) return cudaSuccess;
+    switch (lay.k) {
+        case 1: vnode_sweep_kernel<1><<<blocks, 256, 0, s>>>(lay, d, e, d_rec, src, dst); break;
+        case 2: vnode_sweep_kernel<2><<<blocks, 256, 0, s>>>(lay, d, e, d_rec, src, dst); break;
+        case 3: vnode_sweep_kernel<3><<<blocks, 256, 0, s>>>(lay, d, e, d_rec, src, dst); break;
+        case 4: vnode_sweep_kernel<4><<<blocks, 256, 0, s>>>(lay, d, e, d_rec, src, dst); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace sldg

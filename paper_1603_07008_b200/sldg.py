@@ -27,7 +27,8 @@ EXPORTS = [
     "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
     "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_halo_plan", "sldg_layer_owner",
     "sldg_sweep_kernel", "sldg_vp_create", "sldg_vp_destroy", "sldg_vp_density", "sldg_vp_field",
-    "sldg_vp_step", "sldg_transpose_plan", "sldg_transpose_count",
+    "sldg_vp_step", "sldg_transpose_plan", "sldg_transpose_count", "sldg_advect_vnodes",
+    "sldg_advect_vnodes_device", "sldg_vp_set_nodal",
 ]
 
 
@@ -91,11 +92,14 @@ def lib():
         "sldg_layer_owner": [i64, ctypes.c_int, i64, ctypes.POINTER(ctypes.c_int), i64p],
         "sldg_transpose_plan": [i64, i64, ctypes.c_int, ctypes.c_int, i64p],
         "sldg_transpose_count": [vp, i64p],
+        "sldg_advect_vnodes": [vp, ctypes.c_int, ctypes.c_int, dp],
+        "sldg_advect_vnodes_device": [vp, ctypes.c_int, ctypes.c_int, vp],
         "sldg_vp_create": [vp, ctypes.c_int, ctypes.POINTER(vp)],
         "sldg_vp_destroy": [vp],
         "sldg_vp_density": [vp, dp],
         "sldg_vp_field": [vp, dp, dp, dp, dp],
         "sldg_vp_step": [vp, ctypes.c_double, dp],
+        "sldg_vp_set_nodal": [vp, ctypes.c_int],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -237,6 +241,14 @@ class Grid:
             f = np.ascontiguousarray(field, dtype=np.float64)
             _check(lib().sldg_advect(self.h, int(dim), float(shift), _dp(f), ctypes.c_uint32(field_mask)))
 
+    def advect_vnodes(self, dim: int, vdim: int, nodal_nu):
+        """x-sweep along dim with one CFL number per Gauss node of every v-cell of vdim (NEXT-3)."""
+        f = np.ascontiguousarray(nodal_nu, dtype=np.float64)
+        _check(lib().sldg_advect_vnodes(self.h, int(dim), int(vdim), _dp(f)))
+
+    def advect_vnodes_device(self, dim: int, vdim: int, d_nodal_ptr: int):
+        _check(lib().sldg_advect_vnodes_device(self.h, int(dim), int(vdim), ctypes.c_void_p(d_nodal_ptr)))
+
     def advect_device(self, dim: int, d_field_ptr: int, field_mask: int, shift: float = 0.0):
         _check(lib().sldg_advect_device(self.h, int(dim), float(shift), ctypes.c_void_p(d_field_ptr),
                                         ctypes.c_uint32(field_mask)))
@@ -332,6 +344,10 @@ class VlasovPoisson:
         _check(lib().sldg_vp_field(self.h, None if r is None else _dp(r), _dp(e),
                                    None if coef is None else _dp(coef), _dp(w)))
         return e, coef, float(w[0])
+
+    def set_nodal(self, on: bool = True):
+        """x sweeps by the Gauss-node velocity treatment (NEXT-3) instead of the cell centre."""
+        _check(lib().sldg_vp_set_nodal(self.h, int(bool(on))))
 
     def field_async(self):
         """density + field solve of the grid's f into device buffers only (no host copy)."""

@@ -83,13 +83,15 @@ def test_poisson_2d_parity(n1, n2):
 
 
 @pytest.mark.parametrize("dims,k,dx,steps", [([32, 64], 3, 1, 4), ([16, 12, 10, 8], 2, 2, 2)])
-@pytest.mark.parametrize("force_halo", [False, True])
-def test_strang_step_parity(dims, k, dx, steps, force_halo):
+@pytest.mark.parametrize("force_halo,nodal", [(False, False), (True, False), (False, True)])
+def test_strang_step_parity(dims, k, dx, steps, force_halo, nodal):
     """Each step compared with the oracle step started from the GPU state (only that step's
     rounding differences are measured); Landau-type data with a strong perturbation so that the
     field and the v-sweeps are far from trivial."""
     kw = dict(force_halo=True, max_halo=3) if force_halo else {}
     g, vp, lo, hi = _mk(dims, k, dx, "mixed", **kw)
+    if nodal:
+        vp.set_nodal(True)
     K = k ** len(dims)
     kinds = ["x"] * dx + ["v"] * dx
     terms = sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=0.3, kappa=0.5)
@@ -99,7 +101,7 @@ def test_strang_step_parity(dims, k, dx, steps, force_halo):
     for s in range(steps):
         w = vp.step(0.4, energy=True)
         got = g.get_coeffs()
-        ref, _, wref = ovp.strang_step(cur, dims, k, dx, lo, hi, 0.4, n_double=1)
+        ref, _, wref = ovp.strang_step(cur, dims, k, dx, lo, hi, 0.4, n_double=1, nodal=nodal)
         assert abs(w - wref) <= 1e-12 * wref, (s, w, wref)
         d0 = np.max(np.abs(got[:, 0] - ref[:, 0]))
         assert d0 <= 1e-13 * np.max(np.abs(ref[:, 0])), (s, d0)
@@ -131,8 +133,9 @@ def _rate(ws, dt):
     return np.polyfit(t[pk], np.log(w[pk]), 1)[0] / 2, len(pk)
 
 
-@pytest.mark.parametrize("dims,k,dx", [([32, 128], 3, 1), ([32, 32, 64, 64], 2, 2)])
-def test_landau_damping_on_gpu(dims, k, dx):
+@pytest.mark.parametrize("dims,k,dx,nodal", [([32, 128], 3, 1, False), ([32, 32, 64, 64], 2, 2, False),
+                                             ([32, 64], 3, 1, True)])
+def test_landau_damping_on_gpu(dims, k, dx, nodal):
     """Weak Landau damping (eps = 0.01, kappa = 0.5): the electric energy decays at twice the
     dispersion-relation rate (within 3%), and mass is conserved to fp64 accuracy."""
     from paper_1603_07008_b200 import Grid, VlasovPoisson
@@ -140,6 +143,8 @@ def test_landau_damping_on_gpu(dims, k, dx):
     hi = [2 * np.pi / 0.5] * dx + [6.0] * dx
     g = Grid(dims, k, lo=lo, hi=hi, precision="mixed")
     vp = VlasovPoisson(g, dx)
+    if nodal:  # Gauss-node x sweeps (NEXT-3): half the v cells of the cell-centre run
+        vp.set_nodal(True)
     kinds = ["x"] * dx + ["v"] * dx
     g.fill_separable(sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=0.01, kappa=0.5))
     m0 = g.mass()

@@ -1,0 +1,107 @@
+"""GPU parity of the Gauss-node velocity sweep (sldg_advect_vnodes, NEXT-3) against
+oracle/vnodes.py, and the free-streaming accuracy the nodal treatment buys."""
+import numpy as np
+import pytest
+
+import oracle
+import sldg_inputs
+from oracle import vnodes
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    torch.cuda.set_device(0)
+    yield
+
+
+def _parity(got, ref, K, precision, src, tag):
+    for q in range(K):
+        m = np.max(np.abs(ref[:, q]))
+        d = np.max(np.abs(got[:, q] - ref[:, q]))
+        if precision == "fp64" or q == 0:
+            tol = 1e-13 * max(m, np.max(np.abs(src)))
+        else:
+            tol = 8.0 * float(np.spacing(np.float32(m)))
+        assert d <= tol, f"{tag} slot {q}: {d:.3e} > {tol:.3e}"
+
+
+CASES = [
+    ([16, 12], 3, 0, 1),          # d = 0 (contiguous), v = layer dim
+    ([12, 10], 2, 1, 0),          # sweep along the layer dim, v = dim 0
+    ([8, 6, 10], 3, 0, 2),
+    ([6, 9, 8], 4, 1, 2),         # strided inner sweep
+    ([8, 5, 6, 7], 2, 0, 2),      # 4D: x1 with v1
+    ([5, 8, 4, 6], 3, 1, 3),      # 4D: x2 with v2 (the layer dim)
+]
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+@pytest.mark.parametrize("dims,k,dim,vdim", CASES)
+def test_vnodes_parity(dims, k, dim, vdim, precision):
+    from paper_1603_07008_b200 import Grid
+    D, K = len(dims), k ** len(dims)
+    nd = 1 if precision == "mixed" else K
+    c = sldg_inputs.random_coeffs(dims, k, 21)
+    src = oracle.round_layout(c, K, nd)
+    g = Grid(dims, k, precision=precision)
+    nv = dims[vdim]
+    # wide velocity range (shifts of several cells of both signs) and a cell width in nu large
+    # enough that the nodes of some v-cells straddle an integer (three source offsets)
+    for scale in [0.37, 1.1]:
+        nodal = vnodes.nodal_velocity_field(nv, -3.0, 3.0, k, scale * dims[dim] / 4)
+        g.set_coeffs(c)
+        g.advect_vnodes(dim, vdim, nodal)
+        ref = vnodes.advect_vnodes(src, dims, k, dim, vdim, nodal, n_double=nd)
+        _parity(g.get_coeffs(), ref, K, precision, src, f"dims={dims} dim={dim} vdim={vdim} scale={scale}")
+    g.destroy()
+
+
+def test_vnodes_mass_and_bad_field():
+    from paper_1603_07008_b200 import Grid, SldgError
+    dims, k = [32, 16], 3
+    g = Grid(dims, k, lo=[0, -4], hi=[1, 4])
+    g.fill_random(5)
+    m0 = g.mass()
+    for _ in range(50):
+        g.advect_vnodes(0, 1, vnodes.nodal_velocity_field(16, -4.0, 4.0, k, 3.1))
+    assert abs(g.mass() - m0) <= 1e-13 * abs(m0)
+    bad = vnodes.nodal_velocity_field(16, -4.0, 4.0, k, 1.0)
+    bad[7] = np.nan
+    with pytest.raises(SldgError):
+        g.advect_vnodes(0, 1, bad)
+    with pytest.raises(SldgError):
+        g.advect_vnodes(1, 1, bad)
+    d = torch.tensor(bad, dtype=torch.float64, device="cuda")
+    g.advect_vnodes_device(0, 1, d.data_ptr())
+    with pytest.raises(SldgError):
+        g.mass()  # sticky device error from the non-finite node
+    g.destroy()
+
+
+def test_vnodes_free_streaming_beats_cell_centre():
+    """The GPU path reproduces the oracle's accuracy gain (tests/test_vnodes_oracle.py): one step
+    of free streaming on a 2D grid against the projected exact solution."""
+    from paper_1603_07008_b200 import Grid
+    from tests import test_vnodes_oracle as T
+    k, nx, nv, t = 3, 48, 16, 0.3
+    lox, hix, lov, hiv = 0.0, 1.0, -2.0, 2.0
+    f0 = lambda x, v: np.sin(2 * np.pi * x) * np.exp(-v * v)  # noqa: E731
+    c0 = T._project2d(f0, nx, nv, lox, hix, lov, hiv, k)
+    ce = T._project2d(lambda x, v: f0(x - v * t, v), nx, nv, lox, hix, lov, hiv, k)
+    g = Grid([nx, nv], k, lo=[lox, lov], hi=[hix, hiv], precision="fp64")
+    scale = t / ((hix - lox) / nx)
+    g.set_coeffs(c0)
+    g.advect_vnodes(0, 1, vnodes.nodal_velocity_field(nv, lov, hiv, k, scale))
+    err_node = np.max(np.abs(g.get_coeffs() - ce))
+    vc = lov + (np.arange(nv) + 0.5) * (hiv - lov) / nv
+    g.set_coeffs(c0)
+    g.advect(0, field=vc * scale, field_mask=2)
+    err_cent = np.max(np.abs(g.get_coeffs() - ce))
+    assert err_node < 1e-3 * err_cent * 10 and err_node < 2e-4, (err_node, err_cent)
+    g.destroy()
