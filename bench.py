@@ -418,8 +418,37 @@ def time_vlasov(g, stream, dims, kinds, k, steps=3, dt=0.1):
     field_ms = ev[1].elapsed_time(ev[2]) / steps
     cells, K = int(np.prod(dims)), k ** len(dims)
     w = vp.step(dt, energy=True)
+    # NEXT-3: the same step with Gauss-node x sweeps, and one nodal x1 sweep alone
+    vp.set_nodal(True)
+    vp.step(dt)
+    g.sync()
+    with torch.cuda.stream(stream):
+        ev[0].record(stream)
+    for _ in range(steps):
+        vp.step(dt)
+    with torch.cuda.stream(stream):
+        ev[1].record(stream)
+    g.sync()
+    nodal_ms = ev[0].elapsed_time(ev[1]) / steps
+    g.profile(True)
+    g.kernel_time(reset=True)
+    nv = dims[dx]
+    xg = np.polynomial.legendre.leggauss(k)[0]
+    lo_v, hi_v = -6.0, 6.0
+    hv = (hi_v - lo_v) / nv
+    vc = lo_v + (np.arange(nv) + 0.5) * hv
+    nodal_nu = ((vc[:, None] + xg[None, :] * hv / 2) * dt / (4 * np.pi / dims[0])).reshape(-1)
+    d_nodal = torch.tensor(nodal_nu, dtype=torch.float64, device="cuda")
+    for _ in range(steps):
+        g.advect_vnodes_device(0, dx, d_nodal.data_ptr())
+    g.sync()
+    v_ms, v_n, v_bytes = g.kernel_time(0)
+    g.profile(False)
     vp.destroy()
-    return {"ms_per_step": step_ms, "sweeps_per_step": 3 * dx, "density_and_field_ms": field_ms,
+    nodal = {"ms_per_step": nodal_ms, "x_sweep_kernel_ms": v_ms / max(1, v_n),
+             "x_sweep_gbs": (v_bytes / (v_ms * 1e-3) / 1e9) if v_ms else None,
+             "x_sweep_kernel": "vnode_sweep_kernel (Gauss-node x1 sweep, V7)"}
+    return {"ms_per_step": step_ms, "nodal_x": nodal, "sweeps_per_step": 3 * dx, "density_and_field_ms": field_ms,
             "field_share_of_step": field_ms / step_ms,
             "gdofs_per_sweep": 3 * dx * cells * K / (step_ms * 1e-3) / 1e9,
             "electric_energy": w, "dt": dt,
