@@ -97,6 +97,11 @@ typedef struct {
 /* Every sweep along the layer dim takes the transpose path (testing on one GPU; see
  * sldg_transpose_plan).  Implies the halo layout. */
 #define SLDG_DIST_FORCE_TRANSPOSE 2
+/* world == 1 only: create a one-rank NCCL communicator and send this rank's own halo layers,
+ * transpose blocks and density partials through ncclSend/ncclRecv/ncclAllGather instead of
+ * device copies -- the multi-GPU NCCL code paths (message pointers, counts, pairing order)
+ * exercised on one GPU. */
+#define SLDG_DIST_NCCL_SELF 4
 
 /* Create a grid (zero-filled).  k in 1..SLDG_MAX_K coefficients per dim (the paper's order
  * o = p+1).  dist may be NULL (single GPU).  The device is the caller's current

@@ -245,7 +245,7 @@ sldg_status halo_exchange(sldg_grid g, const Arrays& a, int64_t left, int64_t ri
     };
     std::vector<Xfer> xs = halo_plan(n, g->world, g->rank, L.pad, left, right);
     for (const Xfer& x : xs) {  // layers this rank owns itself (wrap-around): device copies
-        if (x.kind != 2) continue;
+        if (x.kind != 2 || g->nccl_self) continue;
         void *d0, *d1, *s0, *s1;
         size_t c0, c1;
         layer_ptrs(x.slot, &d0, &c0, &d1, &c1);
@@ -254,11 +254,23 @@ sldg_status halo_exchange(sldg_grid g, const Arrays& a, int64_t left, int64_t ri
         if (d1) CU(cudaMemcpyAsync(d1, s1, c1 * 4, cudaMemcpyDeviceToDevice, g->comm_stream));
     }
     bool any = false;
-    for (const Xfer& x : xs) any |= (x.kind != 2);
+    for (const Xfer& x : xs) any |= (x.kind != 2 || g->nccl_self);
     if (!any) return SLDG_OK;
     NC(ncclGroupStart());
     for (const Xfer& x : xs) {
-        if (x.kind == 2) continue;
+        if (x.kind == 2) {
+            if (!g->nccl_self) continue;
+            // SLDG_DIST_NCCL_SELF: the wrap-around copy as a send/recv pair to this rank
+            void *d0, *d1, *s0, *s1;
+            size_t c0, c1;
+            layer_ptrs(x.slot, &d0, &c0, &d1, &c1);
+            layer_ptrs(x.src, &s0, &c0, &s1, &c1);
+            NC(ncclSend(s0, c0, ncclFloat64, g->rank, comm, g->comm_stream));
+            if (s1) NC(ncclSend(s1, c1, ncclFloat32, g->rank, comm, g->comm_stream));
+            NC(ncclRecv(d0, c0, ncclFloat64, g->rank, comm, g->comm_stream));
+            if (d1) NC(ncclRecv(d1, c1, ncclFloat32, g->rank, comm, g->comm_stream));
+            continue;
+        }
         void *p0, *p1;
         size_t c0, c1;
         layer_ptrs(x.slot, &p0, &c0, &p1, &c1);
@@ -351,10 +363,11 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
                            bf(stage_fwd, p), true, st));
         g->launches += 1;
     }
-    if (P > 1) {
+    const bool via_nccl_self = g->nccl_self;  // SLDG_DIST_NCCL_SELF: own block through NCCL too
+    if (P > 1 || via_nccl_self) {
         NC(ncclGroupStart());
         for (int p = 0; p < P; ++p) {
-            if (p == r) continue;
+            if (p == r && !via_nccl_self) continue;
             const int64_t len = plan[p].send_slab_count * Mp;
             if (nl * nd * len) NC(ncclSend(bm(stage_fwd, p), (size_t)(nl * nd * len), ncclFloat64, p, comm, st));
             if (nl * nf * len) NC(ncclSend(bf(stage_fwd, p), (size_t)(nl * nf * len), ncclFloat32, p, comm, st));
@@ -364,7 +377,7 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
         }
         NC(ncclGroupEnd());
     }
-    {
+    if (!via_nccl_self) {
         const int64_t rf = plan[r].recv_layer_first;
         if (nl * nd * lenr)
             CU(cudaMemcpyAsync(Tin.mass + rf * nd * lenr, bm(stage_fwd, r), (size_t)(nl * nd * lenr) * 8,
@@ -412,10 +425,10 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
         if (s2 != SLDG_OK) return s2;
     }
     // inverse: exchange back, self copy, unpack into dst
-    if (P > 1) {
+    if (P > 1 || via_nccl_self) {
         NC(ncclGroupStart());
         for (int p = 0; p < P; ++p) {
-            if (p == r) continue;
+            if (p == r && !via_nccl_self) continue;
             const int64_t rf = plan[p].recv_layer_first, rc = plan[p].recv_layer_count;
             if (rc * nd * lenr) NC(ncclSend(Tout.mass + rf * nd * lenr, (size_t)(rc * nd * lenr), ncclFloat64, p, comm, st));
             if (rc * nf * lenr) NC(ncclSend(Tout.pl + rf * nf * lenr, (size_t)(rc * nf * lenr), ncclFloat32, p, comm, st));
@@ -425,7 +438,7 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
         }
         NC(ncclGroupEnd());
     }
-    {
+    if (!via_nccl_self) {
         const int64_t rf = plan[r].recv_layer_first;
         if (nl * nd * lenr)
             CU(cudaMemcpyAsync(bm(stage_inv, r), Tout.mass + rf * nd * lenr, (size_t)(nl * nd * lenr) * 8,
@@ -776,6 +789,7 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
     }
     g->halo_mode = (world > 1) || (dist && (dist->flags & (SLDG_DIST_FORCE_HALO | SLDG_DIST_FORCE_TRANSPOSE)) && D >= 2);
     g->force_transpose = dist && (dist->flags & SLDG_DIST_FORCE_TRANSPOSE) && D >= 2;
+    g->nccl_self = dist && (dist->flags & SLDG_DIST_NCCL_SELF) && world == 1;
     L.pad = g->halo_mode ? ((dist->max_halo > 0) ? dist->max_halo : 2) : 0;
     L.cells = L.layers * L.L;
     g->rank = rank;
@@ -810,6 +824,15 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
         return bail(fail(SLDG_ENOMEM, "device allocation failed"));
     if (cudaMemsetAsync(g->d_err, 0, sizeof(int), g->stream) != cudaSuccess)
         return bail(fail(SLDG_ECUDA, "memset failed"));
+    if (g->nccl_self) {  // a one-rank communicator: self transfers go through NCCL (testing)
+        ncclUniqueId id;
+        ncclComm_t c;
+        ncclResult_t r = ncclGetUniqueId(&id);
+        if (r == ncclSuccess) r = ncclCommInitRank(&c, 1, id, 0);
+        if (r != ncclSuccess) return bail(fail(SLDG_ENCCL, std::string("ncclCommInitRank(1): ") + ncclGetErrorString(r)));
+        g->comm = c;
+        g->own_comm = true;
+    }
     if (world > 1) {
         if (dist->nccl_comm) {
             g->comm = dist->nccl_comm;

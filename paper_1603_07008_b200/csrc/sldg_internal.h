@@ -190,6 +190,7 @@ struct sldg_grid_s : public sldg::Grid {
     int64_t* d_range = nullptr;
     bool halo_mode = false;  // sweeps along the layer dim read halo layers (sharded, or forced)
     bool force_transpose = false;  // every sweep along the layer dim takes the transpose path
+    bool nccl_self = false;        // world == 1 with a one-rank NCCL communicator: self transfers via NCCL
     void* t_alloc = nullptr;       // transpose path: two slab arrays + receive staging
     size_t t_bytes = 0;
     double* d_tfield = nullptr;    // transpose path: the field restricted to this rank's slab

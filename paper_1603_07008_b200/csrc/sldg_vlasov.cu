@@ -377,11 +377,13 @@ sldg_status vp_density_dev(sldg_vp vp)
     const Arrays& a = g->buf[g->cur];
     cudaStream_t s = g->stream;
     const int64_t part = (int64_t)kVSplit * vp->Kx * vp->Nx;
+    const bool gather = g->world > 1 || g->nccl_self;
     double* mine = vp->d_partial + (g->world > 1 ? (int64_t)g->rank * part : 0);
+    if (g->nccl_self) mine = vp->d_partial + part;  // gathered into slot 0 through NCCL (testing)
     vp_density_partial_kernel<<<dim3(nblk(vp->Nx), vp->Kx, kVSplit), 256, 0, s>>>(L, a, vp->Nx, vp->Kx, mine);
     VCU(cudaGetLastError());
     g->launches += 1;
-    if (g->world > 1) {
+    if (gather) {
         ncclResult_t r = ncclAllGather(mine, vp->d_partial, (size_t)part, ncclFloat64, (ncclComm_t)g->comm, s);
         if (r != ncclSuccess) return set_error(SLDG_ENCCL, std::string("ncclAllGather: ") + ncclGetErrorString(r));
     }
@@ -477,7 +479,7 @@ sldg_status sldg_vp_create(sldg_grid g, int dx, sldg_vp* out)
     auto A = [&](void** p, size_t b) {
         if (st == SLDG_OK) st = vp_alloc(vp, p, b);
     };
-    A((void**)&vp->d_partial, (size_t)part * std::max(1, g->world) * sizeof(double));
+    A((void**)&vp->d_partial, (size_t)part * (std::max(1, g->world) + (g->nccl_self ? 1 : 0)) * sizeof(double));
     A((void**)&vp->d_rho, (size_t)vp->Nx * vp->Kx * sizeof(double));
     A((void**)&vp->d_work, (size_t)(vp->Nx + 1) * sizeof(double));
     A((void**)&vp->d_ecoef, (size_t)vp->Nx * (vp->k + 1) * sizeof(double));

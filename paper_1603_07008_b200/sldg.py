@@ -52,6 +52,7 @@ class Dist(ctypes.Structure):
 
 SLDG_DIST_FORCE_HALO = 1
 SLDG_DIST_FORCE_TRANSPOSE = 2
+SLDG_DIST_NCCL_SELF = 4
 
 
 _lib = None
@@ -166,7 +167,7 @@ class Grid:
 
     def __init__(self, cells, k: int, lo=None, hi=None, precision: str = "mixed",
                  rank: int = 0, world: int = 1, unique_id: bytes | None = None, max_halo: int = 0,
-                 force_halo: bool = False, force_transpose: bool = False):
+                 force_halo: bool = False, force_transpose: bool = False, nccl_self: bool = False):
         cells = [int(c) for c in cells]
         self.D = len(cells)
         self.cells = cells
@@ -186,12 +187,13 @@ class Grid:
             prec = {"mixed": SLDG_MIXED, "fp64": SLDG_FP64}[precision]
         dist_p = None
         self._uid = None
-        if world > 1 or force_halo or force_transpose:
+        if world > 1 or force_halo or force_transpose or nccl_self:
             uid = None
             if world > 1:
                 self._uid = ctypes.create_string_buffer(unique_id, 128)
                 uid = ctypes.cast(self._uid, ctypes.c_void_p)
-            flags = (SLDG_DIST_FORCE_HALO if force_halo else 0) | (SLDG_DIST_FORCE_TRANSPOSE if force_transpose else 0)
+            flags = ((SLDG_DIST_FORCE_HALO if force_halo else 0) | (SLDG_DIST_FORCE_TRANSPOSE if force_transpose else 0)
+                     | (SLDG_DIST_NCCL_SELF if nccl_self else 0))
             self._dist = Dist(rank, world, uid, None, max_halo, flags)
             dist_p = ctypes.byref(self._dist)
         h = ctypes.c_void_p()

@@ -384,9 +384,10 @@ def test_c5_full_size_sampled_lines():
 
 
 # ------------------------------------------------------------------------------ halo path (1 GPU)
+@pytest.mark.parametrize("nccl_self", [False, True])
 @pytest.mark.parametrize("precision", ["mixed", "fp64"])
 @pytest.mark.parametrize("dims,k", [([64, 24], 3), ([32, 6, 20], 2), ([128, 4, 3, 18], 3), ([16, 8, 8, 9], 4)])
-def test_forced_halo_path_matches_oracle(dims, k, precision):
+def test_forced_halo_path_matches_oracle(dims, k, precision, nccl_self):
     """The multi-GPU halo addressing (pad layers, halo exchange plan, interior/boundary launch
     split) run on one GPU: SLDG_DIST_FORCE_HALO makes the rank its own ring neighbour.  Every
     dim is swept (pad > 0 changes every kernel's addressing); the layer-dim sweeps use shifts
@@ -395,7 +396,9 @@ def test_forced_halo_path_matches_oracle(dims, k, precision):
     D, K = len(dims), k ** len(dims)
     c = sldg_inputs.random_coeffs(dims, k, 4242)
     ref_in = oracle_input(c, K, precision)
-    g = _Grid(dims, k, precision=precision, force_halo=True, max_halo=3)
+    # nccl_self: the wrap-around halo layers go through ncclSend/ncclRecv on a one-rank
+    # communicator (the multi-GPU message code path)
+    g = _Grid(dims, k, precision=precision, force_halo=True, max_halo=3, nccl_self=nccl_self)
     rng = np.random.default_rng(len(dims))
     cases = [(d, 1.37, None, 0) for d in range(D)]
     cases += [(D - 1, -2.25, None, 0), (D - 1, 2.0, None, 0), (D - 1, 0.0, rng.uniform(-2.9, 1.9, dims[0]), 1)]
@@ -415,9 +418,10 @@ def test_forced_halo_path_matches_oracle(dims, k, precision):
     g.destroy()
 
 
+@pytest.mark.parametrize("nccl_self", [False, True])
 @pytest.mark.parametrize("precision", ["mixed", "fp64"])
 @pytest.mark.parametrize("dims,k", [([64, 24], 3), ([32, 6, 20], 2), ([8, 5, 3, 11], 3), ([12, 4, 7], 4)])
-def test_forced_transpose_path_matches_oracle(dims, k, precision):
+def test_forced_transpose_path_matches_oracle(dims, k, precision, nccl_self):
     """The transpose path (pack per slab, all-to-all, whole-line local sweep with the field
     restricted to the slab, inverse exchange, unpack) on one GPU (SLDG_DIST_FORCE_TRANSPOSE):
     sweeps along the layer dim with small and large constant shifts and per-line fields over
@@ -425,7 +429,7 @@ def test_forced_transpose_path_matches_oracle(dims, k, precision):
     D, K = len(dims), k ** len(dims)
     c = sldg_inputs.random_coeffs(dims, k, 99)
     ref_in = oracle_input(c, K, precision)
-    g = _Grid(dims, k, precision=precision, force_transpose=True, max_halo=1)
+    g = _Grid(dims, k, precision=precision, force_transpose=True, max_halo=1, nccl_self=nccl_self)
     rng = np.random.default_rng(D * 10 + k)
     nf = dims[0] * dims[D - 2] if D > 2 else dims[0]
     fmask = (1 | (1 << (D - 2))) if D > 2 else 1

@@ -83,12 +83,14 @@ def test_poisson_2d_parity(n1, n2):
 
 
 @pytest.mark.parametrize("dims,k,dx,steps", [([32, 64], 3, 1, 4), ([16, 12, 10, 8], 2, 2, 2)])
-@pytest.mark.parametrize("force_halo,nodal", [(False, False), (True, False), (False, True)])
+@pytest.mark.parametrize("force_halo,nodal", [(False, False), (True, False), (False, True), ("nccl", False)])
 def test_strang_step_parity(dims, k, dx, steps, force_halo, nodal):
     """Each step compared with the oracle step started from the GPU state (only that step's
     rounding differences are measured); Landau-type data with a strong perturbation so that the
     field and the v-sweeps are far from trivial."""
     kw = dict(force_halo=True, max_halo=3) if force_halo else {}
+    if force_halo == "nccl":  # halos and the density all-gather through a one-rank NCCL communicator
+        kw["nccl_self"] = True
     g, vp, lo, hi = _mk(dims, k, dx, "mixed", **kw)
     if nodal:
         vp.set_nodal(True)
