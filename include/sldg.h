@@ -231,22 +231,22 @@ sldg_status sldg_transpose_count(sldg_grid g, int64_t* n);
  * Cheng-Knorr splitting to 1D advections whose CFL number depends on the field
  * (P:269-272).  The paper does not state the field solver; the one here follows S:267-334
  * (V2-V3) and a spectral reading for two space dims (V4).
- * Grid: D = 2 dx dims ordered [x_1..x_dx, v_1..v_dx] (dx = 1 or 2); x_c pairs with v_c.
+ * Grid: D = 2 dx dims ordered [x_1..x_dx, v_1..v_dx] (dx = 1, 2 or 3); x_c pairs with v_c.
  * Density rho[i_x * k^dx + m_x] (i_x = sum_c i_xc S_c over the x dims, m_x likewise):
  *   rho = (prod_c h_vc) sum_{i_v} c_{(i_x, i_v), (m_x, m_v = 0)}                        (V2)
  * Field, dx = 1: d_x E = rho - mean(rho), periodic, zero mean, exact antiderivative of the
  *   DG density per cell (E of degree k per cell; coefficients e[i * (k+1) + n])          (V3)
- * Field, dx = 2: -Lap phi = rho - mean, E = -grad phi, spectral on the cell means
+ * Field, dx = 2, 3: -Lap phi = rho - mean, E = -grad phi, spectral on the cell means
  *   (Nyquist modes of the derivative zeroed), sampled at cell centres                     (V4)
  * E at x-cell centres: e_out[c * N_x + i_x].  Energy: 1/2 int |E|^2 (exact for dx = 1,
- *   cell-centre rule for dx = 2).
+ *   cell-centre rule for dx >= 2).
  * CFL fields (R7, V5): x_c sweeps nu = v_c(cell centre) tau / h_xc over the v_c dim; v_c
  *   sweeps nu = E_c(x-cell centre) tau / h_vc over the x dims.
  * Strang step (V6): x sweeps dt/2; density; field; v sweeps dt; x sweeps dt/2 --
  *   every step on the grid's stream, no host round trip (except the halo range check of a
  *   sharded v sweep).  Distributed grids: the density is summed over ranks in rank order
  *   (ncclAllGather of the partial sums); calls are collective.
- * Errors: EINVAL for a grid that is not [x.., v..] with dx in {1, 2} or for null handles.
+ * Errors: EINVAL for a grid that is not [x.., v..] with dx in {1, 2, 3} or for null handles.
  * Ownership: the driver holds device buffers; the grid must outlive it. */
 typedef struct sldg_vp_s* sldg_vp;
 sldg_status sldg_vp_create(sldg_grid g, int dx, sldg_vp* out);

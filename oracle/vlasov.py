@@ -11,13 +11,13 @@ The paper states the model and the splitting only:
   * the CFL number of a 1D line "can depend ... on the electric field".
 It does not state the field solver.  The rest follows SPEC.md's vlasov_driver,
 with the readings V1-V6 of DESIGN.md section 6c:
-  V1 grid: D = 2 dx, dims [x_1..x_dx, v_1..v_dx]; x_c is advected with v_c, v_c with E_c.
+  V1 grid: D = 2 dx (dx = 1, 2, 3), dims [x_1..x_dx, v_1..v_dx]; x_c is advected with v_c, v_c with E_c.
   V2 density (S:282-288): rho_{i_x, m_x} = (prod_c h_vc) * sum_{i_v} c_{(i_x, i_v), (m_x, 0)}
      (v-integration keeps only the m_v = 0 coefficient, whose Legendre integral is h_v).
   V3 Poisson, dx = 1: d_x E = rho - rho_bar, periodic, zero mean; the cell-wise
      exact antiderivative of the DG density plus cumulative interface constants, then the
      domain mean subtracted.  E is a degree-k polynomial per cell.
-  V4 Poisson, dx = 2 (not in SPEC; reading): -Lap(phi) = rho - rho_bar, E = -grad(phi), solved
+  V4 Poisson, dx = 2, 3 (not in SPEC; reading): -Lap(phi) = rho - rho_bar, E = -grad(phi), solved
      spectrally on the cell means (trigonometric interpolant; Nyquist modes of the derivative
      set to zero); E sampled at cell centres.
   V5 CFL fields (R7, cell-centre reading): x_c sweeps nu = v_c(centre of v_c cell) * tau / h_xc,
@@ -35,7 +35,7 @@ from . import advect as _advect
 
 def _split_dims(dims, dx):
     dims = [int(n) for n in dims]
-    assert len(dims) == 2 * dx and dx in (1, 2)
+    assert len(dims) == 2 * dx and dx in (1, 2, 3)
     return dims[:dx], dims[dx:]
 
 
@@ -90,6 +90,31 @@ def field_centres_1d(e: np.ndarray) -> np.ndarray:
     return eval_legendre_cells(e, 0.0)
 
 
+def poisson_nd(rho_mean: np.ndarray, ns, ls):
+    """V4 for dx = len(ns) >= 2: E = -grad(phi), -Lap(phi) = rho - mean, spectral on the cell
+    means rho_mean[i_1 + n_1 i_2 + ...] (numpy.fft.fftn); returns [E_1, .., E_dx] at the cell
+    centres, same indexing; Nyquist modes of each derivative set to zero."""
+    ns = [int(n) for n in ns]
+    dx = len(ns)
+    r = np.asarray(rho_mean, dtype=np.float64).reshape(ns[::-1])  # axes [i_dx, ..., i_1]
+    rh = np.fft.fftn(r)
+    ks = [2 * np.pi * np.fft.fftfreq(ns[c], d=ls[c] / ns[c]) for c in range(dx)]
+    grids = np.meshgrid(*ks[::-1], indexing="ij")  # grids[a] varies along axis a = dim dx-1-a
+    kk = sum(gq ** 2 for gq in grids)
+    phi = np.zeros_like(rh)
+    nz = kk > 0
+    phi[nz] = rh[nz] / kk[nz]
+    out = []
+    for c in range(dx):
+        dsym = 1j * grids[dx - 1 - c].copy()
+        if ns[c] % 2 == 0:
+            idx = [slice(None)] * dx
+            idx[dx - 1 - c] = ns[c] // 2
+            dsym[tuple(idx)] = 0
+        out.append(np.real(np.fft.ifftn(-dsym * phi)).reshape(-1))
+    return out
+
+
 def poisson_2d(rho_mean: np.ndarray, n1: int, n2: int, l1: float, l2: float):
     """V4: E = -grad(phi), -Lap(phi) = rho - mean, spectral on the cell means rho_mean[i1 + n1 i2];
     returns (E1, E2) at the cell centres, same indexing."""
@@ -133,8 +158,12 @@ def field(c: np.ndarray, dims, k: int, dx: int, lo, hi):
     if dx == 1:
         e = poisson_1d(rho, nx[0], hi[0] - lo[0])
         return [field_centres_1d(e)], energy_1d(e, (hi[0] - lo[0]) / nx[0])
-    e1, e2 = poisson_2d(rho[:, 0], nx[0], nx[1], hi[0] - lo[0], hi[1] - lo[1])
-    return [e1, e2], energy_2d(e1, e2, (hi[0] - lo[0]) / nx[0], (hi[1] - lo[1]) / nx[1])
+    if dx == 2:
+        e1, e2 = poisson_2d(rho[:, 0], nx[0], nx[1], hi[0] - lo[0], hi[1] - lo[1])
+        return [e1, e2], energy_2d(e1, e2, (hi[0] - lo[0]) / nx[0], (hi[1] - lo[1]) / nx[1])
+    es = poisson_nd(rho[:, 0], nx, [hi[c] - lo[c] for c in range(dx)])
+    hprod = np.prod([(hi[c] - lo[c]) / nx[c] for c in range(dx)])
+    return es, 0.5 * hprod * float(sum(np.sum(e ** 2) for e in es))
 
 
 def x_field(dims, dx: int, lo, hi, c: int, tau: float) -> np.ndarray:

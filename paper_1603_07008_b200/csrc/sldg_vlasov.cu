@@ -193,23 +193,6 @@ __device__ __forceinline__ void twiddle(int64_t a, int64_t b, int64_t n, double 
     *s = sign * sv;
 }
 
-// A[k1 + n1 i2] = sum_i1 rho_mean(i1, i2) e^{-2 pi i k1 i1 / n1}   (rho_mean = rho[(i1 + n1 i2) Kx])
-__global__ void vp_dft_rows_kernel(const double* rho, int Kx, int64_t n1, int64_t n2, double2* A)
-{
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n1 * n2) return;
-    const int64_t k1 = t % n1, i2 = t / n1;
-    double re = 0.0, im = 0.0;
-    for (int64_t i1 = 0; i1 < n1; ++i1) {
-        double c, s;
-        twiddle(k1, i1, n1, -1.0, &c, &s);
-        const double r = rho[(i1 + n1 * i2) * Kx];
-        re += r * c;
-        im += r * s;
-    }
-    A[t] = make_double2(re, im);
-}
-
 // signed angular frequency of index j on a periodic interval of n cells and length len
 __device__ __forceinline__ double vp_freq(int64_t j, int64_t n, double len)
 {
@@ -217,89 +200,87 @@ __device__ __forceinline__ double vp_freq(int64_t j, int64_t n, double len)
     return 2.0 * M_PI * (double)js / len;
 }
 
-// B = column DFT of A; then Ehat_c = -i kappa_c phi_hat, phi_hat = B / |kappa|^2 (0 at kappa = 0),
-// with the Nyquist derivative modes zeroed (V4).  Out: E1hat, E2hat [k1 + n1 k2].
-__global__ void vp_dft_cols_solve_kernel(const double2* A, int64_t n1, int64_t n2, double l1, double l2,
-                                         double2* E1h, double2* E2h)
+// F[t] = rho_mean(t) + 0i  (rho_mean = rho[t * Kx], the P_0 coefficient of x-cell t)
+__global__ void vp_dft_load_kernel(const double* rho, int Kx, int64_t N, double2* F)
 {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n1 * n2) return;
-    const int64_t k1 = t % n1, k2 = t / n1;
+    if (t < N) F[t] = make_double2(rho[t * Kx], 0.0);
+}
+
+// one direct DFT pass along a dim of extent n and element stride `stride` of an N-element
+// complex array: out[.. k ..] = sum_i in[.. i ..] e^{sign 2 pi i (k i mod n) / n}
+__global__ void vp_dft_pass_kernel(const double2* in, double2* out, int64_t N, int64_t n, int64_t stride,
+                                   double sign)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    const int64_t kk = (t / stride) % n;
+    const int64_t base = t - kk * stride;
     double re = 0.0, im = 0.0;
-    for (int64_t i2 = 0; i2 < n2; ++i2) {
+    for (int64_t i = 0; i < n; ++i) {
         double c, s;
-        twiddle(k2, i2, n2, -1.0, &c, &s);
-        const double2 a = A[k1 + n1 * i2];
+        twiddle(kk, i, n, sign, &c, &s);
+        const double2 a = in[base + i * stride];
         re += a.x * c - a.y * s;
         im += a.x * s + a.y * c;
     }
-    const double q1 = vp_freq(k1, n1, l1), q2 = vp_freq(k2, n2, l2);
-    const double kk = q1 * q1 + q2 * q2;
+    out[t] = make_double2(re, im);
+}
+
+// Ehat_c = -i kappa_c phi_hat, phi_hat = F / |kappa|^2 (0 at kappa = 0); Nyquist modes of the
+// derivative along c zeroed (V4).  dims / lengths of the dx x dims, dim 0 fastest.
+struct VpDims {
+    int dx;
+    int64_t n[3];
+    double len[3];
+};
+__global__ void vp_solve_kernel(const double2* F, int64_t N, VpDims g, int c, double2* E)
+{
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    int64_t rem = t;
+    double kk = 0.0, qc = 0.0;
+    bool nyq = false;
+    for (int a = 0; a < g.dx; ++a) {
+        const int64_t j = rem % g.n[a];
+        rem /= g.n[a];
+        const double q = vp_freq(j, g.n[a], g.len[a]);
+        kk += q * q;
+        if (a == c) {
+            qc = q;
+            nyq = (g.n[a] % 2 == 0) && (j == g.n[a] / 2);
+        }
+    }
+    const double d = nyq ? 0.0 : qc;
     double pr = 0.0, pi = 0.0;
     if (kk > 0.0) {
-        pr = re / kk;
-        pi = im / kk;
+        pr = F[t].x / kk;
+        pi = F[t].y / kk;
     }
-    const double d1 = (n1 % 2 == 0 && k1 == n1 / 2) ? 0.0 : q1;
-    const double d2 = (n2 % 2 == 0 && k2 == n2 / 2) ? 0.0 : q2;
-    // -i d phi = (d pi, -d pr)
-    E1h[t] = make_double2(d1 * pi, -d1 * pr);
-    E2h[t] = make_double2(d2 * pi, -d2 * pr);
+    E[t] = make_double2(d * pi, -d * pr);  // -i d (pr + i pi)
 }
 
-// T_c[k1 + n1 i2] = sum_k2 Ehat_c(k1, k2) e^{+2 pi i k2 i2 / n2}
-__global__ void vp_idft_cols_kernel(const double2* E1h, const double2* E2h, int64_t n1, int64_t n2, double2* T1,
-                                    double2* T2)
+// ec[t] = Re(A[t]) / N
+__global__ void vp_real_scale_kernel(const double2* A, int64_t N, double* ec)
 {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= n1 * n2) return;
-    const int64_t k1 = t % n1, i2 = t / n1;
-    double r1 = 0.0, j1 = 0.0, r2 = 0.0, j2 = 0.0;
-    for (int64_t k2 = 0; k2 < n2; ++k2) {
-        double c, s;
-        twiddle(k2, i2, n2, 1.0, &c, &s);
-        const double2 a = E1h[k1 + n1 * k2], b = E2h[k1 + n1 * k2];
-        r1 += a.x * c - a.y * s;
-        j1 += a.x * s + a.y * c;
-        r2 += b.x * c - b.y * s;
-        j2 += b.x * s + b.y * c;
-    }
-    T1[t] = make_double2(r1, j1);
-    T2[t] = make_double2(r2, j2);
+    if (t < N) ec[t] = A[t].x / (double)N;
 }
 
-// E_c(i1, i2) = Re sum_k1 T_c(k1, i2) e^{+2 pi i k1 i1 / n1} / (n1 n2) -> ec[c * N + i1 + n1 i2]
-__global__ void vp_idft_rows_kernel(const double2* T1, const double2* T2, int64_t n1, int64_t n2, double* ec)
-{
-    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t N = n1 * n2;
-    if (t >= N) return;
-    const int64_t i1 = t % n1, i2 = t / n1;
-    double r1 = 0.0, r2 = 0.0;
-    for (int64_t k1 = 0; k1 < n1; ++k1) {
-        double c, s;
-        twiddle(k1, i1, n1, 1.0, &c, &s);
-        const double2 a = T1[k1 + n1 * i2], b = T2[k1 + n1 * i2];
-        r1 += a.x * c - a.y * s;
-        r2 += b.x * c - b.y * s;
-    }
-    ec[t] = r1 / (double)N;
-    ec[N + t] = r2 / (double)N;
-}
-
-// energy = 1/2 h1 h2 sum (E1^2 + E2^2), one CTA, fixed order
-__global__ void vp_energy2d_kernel(const double* ec, int64_t N, double h1h2, double* energy)
+// energy = 1/2 (prod h) sum_c sum (E_c^2), one CTA, fixed order
+__global__ void vp_energy_nd_kernel(const double* ec, int64_t N, int dx, double hprod, double* energy)
 {
     __shared__ double sh[256];
     const int tid = threadIdx.x, nt = blockDim.x;
     double s = 0.0;
-    for (int64_t i = tid; i < N; i += nt) s += ec[i] * ec[i] + ec[N + i] * ec[N + i];
+    for (int64_t i = tid; i < N; i += nt)
+        for (int c = 0; c < dx; ++c) s += ec[c * N + i] * ec[c * N + i];
     sh[tid] = s;
     __syncthreads();
     if (tid == 0) {
         double t = 0.0;
         for (int j = 0; j < nt; ++j) t += sh[j];
-        *energy = 0.5 * h1h2 * t;
+        *energy = 0.5 * hprod * t;
     }
 }
 
@@ -338,7 +319,7 @@ struct sldg_vp_s {
     sldg_grid g = nullptr;
     int dx = 1, k = 1, Kx = 1;
     bool nodal = false;        // x sweeps by the Gauss-node velocity treatment (V7)
-    int64_t nx[2] = {1, 1}, Nx = 1;
+    int64_t nx[3] = {1, 1, 1}, Nx = 1;
     double hv = 1.0;           // prod_c h_vc
     double* d_partial = nullptr;   // [world][kVSplit][Kx][Nx]
     double* d_rho = nullptr;       // [Nx][Kx]
@@ -346,9 +327,10 @@ struct sldg_vp_s {
     double* d_ecoef = nullptr;     // dx = 1: [Nx][k+1]
     double* d_ec = nullptr;        // [dx][Nx] centre values
     double* d_energy = nullptr;
-    double2* d_c[4] = {nullptr, nullptr, nullptr, nullptr};  // dx = 2: DFT work [Nx] each
-    double* d_nux[2] = {nullptr, nullptr};  // x_c sweep fields [n_vc]
-    double* d_nuv[2] = {nullptr, nullptr};  // v_c sweep fields [Nx]
+    double2* d_c[2] = {nullptr, nullptr};  // dx >= 2: DFT work [Nx] each
+    double2* d_ctmp = nullptr;
+    double* d_nux[3] = {nullptr, nullptr, nullptr};  // x_c sweep fields [n_vc] (nodal: [n_vc k])
+    double* d_nuv[3] = {nullptr, nullptr, nullptr};  // v_c sweep fields [Nx]
     std::vector<void*> allocs;
 };
 
@@ -407,15 +389,45 @@ sldg_status vp_field_dev(sldg_vp vp)
         g->launches += 1;
         return SLDG_OK;
     }
-    const int64_t n1 = vp->nx[0], n2 = vp->nx[1], N = vp->Nx;
-    const double l1 = g->hi[0] - g->lo[0], l2 = g->hi[1] - g->lo[1];
-    vp_dft_rows_kernel<<<nblk(N), 256, 0, s>>>(vp->d_rho, vp->Kx, n1, n2, vp->d_c[0]);
-    vp_dft_cols_solve_kernel<<<nblk(N), 256, 0, s>>>(vp->d_c[0], n1, n2, l1, l2, vp->d_c[1], vp->d_c[2]);
-    vp_idft_cols_kernel<<<nblk(N), 256, 0, s>>>(vp->d_c[1], vp->d_c[2], n1, n2, vp->d_c[0], vp->d_c[3]);
-    vp_idft_rows_kernel<<<nblk(N), 256, 0, s>>>(vp->d_c[0], vp->d_c[3], n1, n2, vp->d_ec);
-    vp_energy2d_kernel<<<1, 256, 0, s>>>(vp->d_ec, N, g->h[0] * g->h[1], vp->d_energy);
+    const int64_t N = vp->Nx;
+    VpDims gd{};
+    gd.dx = vp->dx;
+    double hprod = 1.0;
+    for (int c = 0; c < vp->dx; ++c) {
+        gd.n[c] = vp->nx[c];
+        gd.len[c] = g->hi[c] - g->lo[c];
+        hprod *= g->h[c];
+    }
+    // forward transform of the cell means, one pass per x dim (ping-pong d_c[0] <-> d_c[1])
+    vp_dft_load_kernel<<<nblk(N), 256, 0, s>>>(vp->d_rho, vp->Kx, N, vp->d_c[0]);
+    int cur = 0;
+    int64_t stride = 1;
+    for (int c = 0; c < vp->dx; ++c) {
+        vp_dft_pass_kernel<<<nblk(N), 256, 0, s>>>(vp->d_c[cur], vp->d_c[1 - cur], N, vp->nx[c], stride, -1.0);
+        cur = 1 - cur;
+        stride *= vp->nx[c];
+    }
+    g->launches += 1 + vp->dx;
+    // per component: solve into the spare buffer, inverse passes, real part
+    const int F = cur;  // spectrum
+    for (int c = 0; c < vp->dx; ++c) {
+        double2* a = vp->d_c[1 - F];
+        double2* b = vp->d_ctmp;
+        vp_solve_kernel<<<nblk(N), 256, 0, s>>>(vp->d_c[F], N, gd, c, a);
+        int64_t st2 = 1;
+        for (int e = 0; e < vp->dx; ++e) {
+            vp_dft_pass_kernel<<<nblk(N), 256, 0, s>>>(a, b, N, vp->nx[e], st2, 1.0);
+            double2* t = a;
+            a = b;
+            b = t;
+            st2 *= vp->nx[e];
+        }
+        vp_real_scale_kernel<<<nblk(N), 256, 0, s>>>(a, N, vp->d_ec + (int64_t)c * N);
+        g->launches += 2 + vp->dx;
+    }
+    vp_energy_nd_kernel<<<1, 256, 0, s>>>(vp->d_ec, N, vp->dx, hprod, vp->d_energy);
     VCU(cudaGetLastError());
-    g->launches += 5;
+    g->launches += 1;
     return SLDG_OK;
 }
 
@@ -459,14 +471,15 @@ sldg_status sldg_vp_create(sldg_grid g, int dx, sldg_vp* out)
     if (!g || !out) return set_error(SLDG_EINVAL, "null argument");
     *out = nullptr;
     const Layout& L = g->lay;
-    if ((dx != 1 && dx != 2) || L.D != 2 * dx) return set_error(SLDG_EINVAL, "grid must be [x.., v..] with dx in {1, 2}");
+    if (dx < 1 || dx > 3 || L.D != 2 * dx) return set_error(SLDG_EINVAL, "grid must be [x.., v..] with dx in {1, 2, 3}");
     if (L.prec == SLDG_GENERAL) return set_error(SLDG_EINVAL, "general precision layouts are 1D only");
     sldg_vp vp = new (std::nothrow) sldg_vp_s;
     if (!vp) return set_error(SLDG_ENOMEM, "host allocation");
     vp->g = g;
     vp->dx = dx;
     vp->k = L.k;
-    vp->Kx = (dx == 1) ? L.k : L.k * L.k;
+    vp->Kx = 1;
+    for (int c = 0; c < dx; ++c) vp->Kx *= L.k;
     vp->Nx = 1;
     vp->hv = 1.0;
     for (int c = 0; c < dx; ++c) {
@@ -485,8 +498,10 @@ sldg_status sldg_vp_create(sldg_grid g, int dx, sldg_vp* out)
     A((void**)&vp->d_ecoef, (size_t)vp->Nx * (vp->k + 1) * sizeof(double));
     A((void**)&vp->d_ec, (size_t)dx * vp->Nx * sizeof(double));
     A((void**)&vp->d_energy, sizeof(double));
-    if (dx == 2)
-        for (int i = 0; i < 4; ++i) A((void**)&vp->d_c[i], (size_t)vp->Nx * sizeof(double2));
+    if (dx >= 2) {
+        for (int i = 0; i < 2; ++i) A((void**)&vp->d_c[i], (size_t)vp->Nx * sizeof(double2));
+        A((void**)&vp->d_ctmp, (size_t)vp->Nx * sizeof(double2));
+    }
     for (int c = 0; c < dx; ++c) {
         A((void**)&vp->d_nux[c], (size_t)L.n[dx + c] * L.k * sizeof(double));
         A((void**)&vp->d_nuv[c], (size_t)vp->Nx * sizeof(double));
@@ -502,7 +517,9 @@ sldg_status sldg_vp_create(sldg_grid g, int dx, sldg_vp* out)
 sldg_status sldg_vp_destroy(sldg_vp vp)
 {
     if (!vp) return SLDG_OK;
-    if (vp->g) cudaStreamSynchronize(vp->g->stream);
+    // no access to vp->g here: the grid may already be gone (the binding destroys drivers
+    // first, but a C caller may not); cudaFree synchronises with outstanding device work
+    cudaDeviceSynchronize();
     for (void* p : vp->allocs) cudaFree(p);
     delete vp;
     return SLDG_OK;

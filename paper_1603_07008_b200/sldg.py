@@ -8,6 +8,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import weakref
 
 import numpy as np
 
@@ -203,6 +204,7 @@ class Grid:
             _check(lib().sldg_create_ex(ctypes.byref(gd), self.k, ctypes.byref(dom), int(n_double), dist_p,
                                         ctypes.byref(h)))
         self.h = h
+        self._dependents = weakref.WeakSet()
         fl, nl = ctypes.c_int64(), ctypes.c_int64()
         _check(lib().sldg_shard_info(self.h, ctypes.byref(fl), ctypes.byref(nl)))
         self.first_layer, self.n_layers = fl.value, nl.value
@@ -213,6 +215,8 @@ class Grid:
 
     # -- lifecycle
     def destroy(self):
+        for dep in list(getattr(self, "_dependents", ())):
+            dep.destroy()
         if getattr(self, "h", None):
             lib().sldg_destroy(self.h)
             self.h = None
@@ -319,6 +323,7 @@ class VlasovPoisson:
         h = ctypes.c_void_p()
         _check(lib().sldg_vp_create(grid.h, self.dx, ctypes.byref(h)))
         self.h = h
+        grid._dependents.add(self)  # destroyed before the grid (sldg_vp_* hold the grid pointer)
 
     def destroy(self):
         if self.h:

@@ -139,6 +139,32 @@ def test_poisson_2d_modes_closed_form():
         assert np.max(np.abs(e2 - k2 / kk * s.reshape(-1))) <= 1e-15
 
 
+def test_poisson_3d_modes_closed_form():
+    """The dx = 3 solve (numpy fftn) on single Fourier modes: E = (kappa/|kappa|^2) eps fac
+    sin(kappa.x_c) with the product of the three cell-mean sinc factors; and the 2D wrapper
+    agrees with the N-D routine."""
+    ns, ls = [8, 6, 10], [4 * np.pi, 2 * np.pi, 3.0]
+    hs = [ls[c] / ns[c] for c in range(3)]
+    xc = [(np.arange(ns[c]) + 0.5) * hs[c] for c in range(3)]
+    X = np.meshgrid(*xc[::-1], indexing="ij")  # [i3, i2, i1]
+    X3, X2, X1 = X
+    sinc = lambda z: 1.0 if z == 0 else np.sin(z) / z  # noqa: E731
+    for a in [(1, 0, 0), (0, 2, 1), (3, -1, 2), (0, 0, 1)]:
+        kv = [2 * np.pi * a[c] / ls[c] for c in range(3)]
+        fac = np.prod([sinc(kv[c] * hs[c] / 2) for c in range(3)])
+        ph = kv[0] * X1 + kv[1] * X2 + kv[2] * X3
+        rho = 1.0 + 0.03 * fac * np.cos(ph)
+        es = vp.poisson_nd(rho.reshape(-1), ns, ls)
+        kk = sum(q * q for q in kv)
+        for c in range(3):
+            want = (kv[c] / kk * 0.03 * fac * np.sin(ph)).reshape(-1)
+            assert np.max(np.abs(es[c] - want)) <= 1e-15
+    r2 = np.random.default_rng(1).standard_normal(12 * 10)
+    e1, e2 = vp.poisson_2d(r2, 12, 10, 3.0, 2.0)
+    f1, f2 = vp.poisson_nd(r2, [12, 10], [3.0, 2.0])
+    assert np.max(np.abs(e1 - f1)) <= 1e-15 and np.max(np.abs(e2 - f2)) <= 1e-15
+
+
 def test_poisson_2d_reduces_to_1d():
     """A density constant along x2 gives E2 = 0 and, for a pure Fourier mode, E1 equal to the 1D
     spectral answer -- consistency between the two solvers at cell centres up to the DG/spectral
@@ -184,7 +210,7 @@ def test_strang_homogeneous_state_is_stationary():
     """f = g(v), homogeneous in x: rho is uniform so E = 0, the x-translations of an x-constant
     function are exact and the v-sweeps shift by nu = 0 (copies): the Strang step leaves f
     unchanged up to rounding (equilibrium of the Vlasov-Poisson system)."""
-    for dx, dims in [(1, [8, 16]), (2, [4, 6, 8, 10])]:
+    for dx, dims in [(1, [8, 16]), (2, [4, 6, 8, 10]), (3, [3, 4, 2, 4, 5, 4])]:
         k = 2
         lo = [0.0] * dx + [-4.0] * dx
         hi = [1.0] * dx + [4.0] * dx
