@@ -192,6 +192,22 @@ int64_t sldg_launch_count(sldg_grid g);
  * kernels. */
 const char* sldg_sweep_kernel(sldg_grid g, int dim);
 
+/* ---- CUDA graphs ------------------------------------------------------------------------ */
+/* Capture a sequence of ASYNCHRONOUS calls on this grid (sldg_advect with field == NULL,
+ * sldg_advect_device, sldg_advect_vnodes_device, sldg_fill_*) into a CUDA graph and replay
+ * it with one launch: for small grids whose sweeps are shorter than the host's per-call cost.
+ * Nothing runs during the capture.  A replay must start on the buffer the capture started on
+ * (an odd number of sweeps flips the ping-pong buffer: capture two steps).  Device shift
+ * fields must stay valid and are read at replay time.  Errors: EINVAL (capture already open /
+ * not open, host field during capture, wrong current buffer at launch), ENOTSUP (sharded or
+ * forced-halo grids: their layer-dim sweeps synchronise the host), ECUDA (a blocking call was
+ * made inside the capture; the capture is then invalid). */
+typedef struct sldg_graph_s* sldg_graph;
+sldg_status sldg_graph_begin(sldg_grid g);
+sldg_status sldg_graph_end(sldg_grid g, sldg_graph* out);
+sldg_status sldg_graph_launch(sldg_graph gr);
+sldg_status sldg_graph_destroy(sldg_graph gr);
+
 /* ---- distributed helpers ---------------------------------------------------------------- */
 /* Write a fresh 128-byte ncclUniqueId into out128 (call on rank 0, broadcast it). */
 sldg_status sldg_nccl_unique_id(void* out128);

@@ -937,7 +937,89 @@ sldg_status sldg_get_coeffs(sldg_grid g, double* dst, int64_t first_cell, int64_
 sldg_status sldg_advect(sldg_grid g, int dim, double shift, const double* field, uint32_t field_mask)
 {
     if (!g) return fail(SLDG_EINVAL, "null grid");
+    if (field && g->capturing)
+        return fail(SLDG_EINVAL, "a host shift field cannot be captured in a graph: use sldg_advect_device");
     return advect_impl(g, dim, shift, field, false, field_mask);
+}
+
+// ---- CUDA graphs of asynchronous call sequences (launch-bound small grids) ------------------
+struct sldg_graph_s {
+    sldg_grid g = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int cur_begin = 0, cur_end = 0;
+    int64_t launches = 0;
+};
+
+sldg_status sldg_graph_begin(sldg_grid g)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    if (g->capturing) return fail(SLDG_EINVAL, "a capture is already open");
+    if (g->halo_mode) return fail(SLDG_ENOTSUP, "graph capture of a sharded grid (halo sweeps sync the host)");
+    CU(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
+    g->capturing = true;
+    g->cap_cur = g->cur;
+    g->cap_launches = g->launches;
+    g->cap_profile = g->profile;
+    g->profile = false;  // per-sweep events are bookkept on the host: not inside a graph
+    g->w_const = false;  // the captured sequence builds its own weights
+    return SLDG_OK;
+}
+
+sldg_status sldg_graph_end(sldg_grid g, sldg_graph* out)
+{
+    if (!g || !out) return fail(SLDG_EINVAL, "null argument");
+    if (!g->capturing) return fail(SLDG_EINVAL, "no capture is open");
+    *out = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaError_t e = cudaStreamEndCapture(g->stream, &graph);
+    g->capturing = false;
+    g->profile = g->cap_profile;
+    g->w_const = false;
+    const int cur_end = g->cur;
+    const int64_t nl = g->launches - g->cap_launches;
+    g->cur = g->cap_cur;  // nothing ran: the captured sweeps run at sldg_graph_launch
+    g->launches = g->cap_launches;
+    if (e != cudaSuccess) return fail(SLDG_ECUDA, std::string("cudaStreamEndCapture: ") + cudaGetErrorString(e));
+    sldg_graph gr = new (std::nothrow) sldg_graph_s;
+    if (!gr) {
+        cudaGraphDestroy(graph);
+        return fail(SLDG_ENOMEM, "host allocation");
+    }
+    e = cudaGraphInstantiate(&gr->exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) {
+        delete gr;
+        return fail(SLDG_ECUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(e));
+    }
+    gr->g = g;
+    gr->cur_begin = g->cap_cur;
+    gr->cur_end = cur_end;
+    gr->launches = nl;
+    *out = gr;
+    return SLDG_OK;
+}
+
+sldg_status sldg_graph_launch(sldg_graph gr)
+{
+    if (!gr) return fail(SLDG_EINVAL, "null graph");
+    sldg_grid g = gr->g;
+    if (g->cur != gr->cur_begin)
+        return fail(SLDG_EINVAL, "the grid's current buffer differs from the one the graph was captured on "
+                                 "(an odd number of sweeps: capture two steps)");
+    CU(cudaGraphLaunch(gr->exec, g->stream));
+    g->cur = gr->cur_end;
+    g->launches += gr->launches;
+    g->w_const = false;
+    return SLDG_OK;
+}
+
+sldg_status sldg_graph_destroy(sldg_graph gr)
+{
+    if (!gr) return SLDG_OK;
+    if (gr->g) cudaStreamSynchronize(gr->g->stream);
+    if (gr->exec) cudaGraphExecDestroy(gr->exec);
+    delete gr;
+    return SLDG_OK;
 }
 
 sldg_status sldg_advect_device(sldg_grid g, int dim, double shift, const double* d_field, uint32_t field_mask)

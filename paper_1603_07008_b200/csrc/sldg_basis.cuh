@@ -5,7 +5,8 @@
 // build_ab: A_jl = (2j+1)/2 int_{-1}^{2a-1} P_l(xi+2-2a) P_j(xi) dxi, B_jl = (2j+1)/2
 // int_{2a-1}^{1} P_l(xi-2a) P_j(xi) dxi (P:259-268 SS II-A), each by a k-point
 // Gauss-Legendre rule mapped to the sub-interval (exact for the degree <= 2k-2 integrand), mass
-// row in closed form (reading R3).
+// row in closed form (reading R3).  The Gauss nodes/weights come from the host (GaussTab,
+// sldg_kernels.cu gauss_table) as a kernel parameter.
 #pragma once
 #include <math.h>
 
@@ -17,99 +18,98 @@ __device__ __forceinline__ void dev_legendre(int pmax, double x, double* P)
 {
     P[0] = 1.0;
     if (pmax > 0) P[1] = x;
+#pragma unroll
     for (int n = 2; n <= pmax; ++n) P[n] = ((2 * n - 1) * x * P[n - 1] - (n - 1) * P[n - 2]) / n;
 }
 
-// Gauss-Legendre nodes/weights on [-1,1] by Newton on P_n (roots symmetric; compute the
-// non-negative half and mirror).
-__device__ __forceinline__ void dev_gauss(int n, double* x, double* w)
+// KK compile-time: the Legendre values and both accumulators live in registers (a runtime k
+// put them in local memory and made every += a dependent global read-modify-write of A / B).
+template <int KK>
+__device__ __forceinline__ void build_ab_regs(double a, const double* xg, const double* wg, double* Al, double* Bl)
 {
-    const double kPi = 3.141592653589793238462643;
-    for (int i = 0; i < (n + 1) / 2; ++i) {
-        double z = cos(kPi * (i + 0.75) / (n + 0.5));
-        double pn = 0.0, dpn = 1.0;
-        for (int it = 0; it < 60; ++it) {
-            double p0 = 1.0, p1 = z;
-            for (int m = 2; m <= n; ++m) {
-                double p2 = ((2 * m - 1) * z * p1 - (m - 1) * p0) / m;
-                p0 = p1;
-                p1 = p2;
-            }
-            pn = (n == 1) ? z : p1;
-            double pm1 = (n == 1) ? 1.0 : p0;
-            dpn = n * (pm1 - z * pn) / (1.0 - z * z);
-            double dz = pn / dpn;
-            z -= dz;
-            if (fabs(dz) < 1e-17) break;
-        }
-        {  // derivative at the converged node
-            double p0 = 1.0, p1 = z;
-            for (int m = 2; m <= n; ++m) {
-                double p2 = ((2 * m - 1) * z * p1 - (m - 1) * p0) / m;
-                p0 = p1;
-                p1 = p2;
-            }
-            double pm1 = (n == 1) ? 1.0 : p0;
-            double pnn = (n == 1) ? z : p1;
-            dpn = n * (pm1 - z * pnn) / (1.0 - z * z);
-        }
-        double wi = 2.0 / ((1.0 - z * z) * dpn * dpn);
-        x[i] = -z;
-        w[i] = wi;
-        x[n - 1 - i] = z;
-        w[n - 1 - i] = wi;
+    double Pj[KK + 2], Pl[KK + 2];
+#pragma unroll
+    for (int j = 0; j < KK * KK; ++j) {
+        Al[j] = 0.0;
+        Bl[j] = 0.0;
     }
-    if (n & 1) x[n / 2] = 0.0;
-}
-
-
-__device__ __forceinline__ void build_ab(int k, double a, double* A, double* B)
-{
-    double xg[kMaxK], wg[kMaxK], Pj[kMaxK + 2], Pl[kMaxK + 2];
-    dev_gauss(k, xg, wg);
-    for (int j = 0; j < k * k; ++j) {
-        A[j] = 0.0;
-        B[j] = 0.0;
-    }
-    for (int g = 0; g < k; ++g) {
+#pragma unroll
+    for (int g = 0; g < KK; ++g) {
         // A: xi in [-1, 2a-1] -> xi = (a - 1) + a t ; integrand P_l(xi + 2 - 2a) P_j(xi)
         double xi = (a - 1.0) + a * xg[g];
-        dev_legendre(k - 1, xi, Pj);
-        dev_legendre(k - 1, xi + 2.0 - 2.0 * a, Pl);
-        for (int j = 0; j < k; ++j)
-            for (int l = 0; l < k; ++l) A[j * k + l] += wg[g] * (Pj[j] * Pl[l]);
+        dev_legendre(KK - 1, xi, Pj);
+        dev_legendre(KK - 1, xi + 2.0 - 2.0 * a, Pl);
+#pragma unroll
+        for (int j = 0; j < KK; ++j)
+#pragma unroll
+            for (int l = 0; l < KK; ++l) Al[j * KK + l] += wg[g] * (Pj[j] * Pl[l]);
         // B: xi in [2a-1, 1] -> xi = a + (1 - a) t ; integrand P_l(xi - 2a) P_j(xi)
         xi = a + (1.0 - a) * xg[g];
-        dev_legendre(k - 1, xi, Pj);
-        dev_legendre(k - 1, xi - 2.0 * a, Pl);
-        for (int j = 0; j < k; ++j)
-            for (int l = 0; l < k; ++l) B[j * k + l] += wg[g] * (Pj[j] * Pl[l]);
+        dev_legendre(KK - 1, xi, Pj);
+        dev_legendre(KK - 1, xi - 2.0 * a, Pl);
+#pragma unroll
+        for (int j = 0; j < KK; ++j)
+#pragma unroll
+            for (int l = 0; l < KK; ++l) Bl[j * KK + l] += wg[g] * (Pj[j] * Pl[l]);
     }
-    for (int j = 0; j < k; ++j) {
-        double sa = 0.5 * (2 * j + 1) * a, sb = 0.5 * (2 * j + 1) * (1.0 - a);
-        for (int l = 0; l < k; ++l) {
-            A[j * k + l] *= sa;
-            B[j * k + l] *= sb;
+#pragma unroll
+    for (int j = 0; j < KK; ++j) {
+        const double sa = 0.5 * (2 * j + 1) * a, sb = 0.5 * (2 * j + 1) * (1.0 - a);
+#pragma unroll
+        for (int l = 0; l < KK; ++l) {
+            Al[j * KK + l] *= sa;
+            Bl[j * KK + l] *= sb;
         }
     }
     // mass row, closed form (reading R3): int_x^1 P_l = -(P_{l+1}(x) - P_{l-1}(x))/(2l+1)
     {
-        double P[kMaxK + 2];
-        dev_legendre(k, 1.0 - 2.0 * a, P);
-        for (int l = 1; l < k; ++l) {
-            double v = -(P[l + 1] - P[l - 1]) / (2.0 * (2 * l + 1));
-            A[l] = v;
-            B[l] = -v;
+        double P[KK + 2];
+        dev_legendre(KK, 1.0 - 2.0 * a, P);
+#pragma unroll
+        for (int l = 1; l < KK; ++l) {
+            const double v = -(P[l + 1] - P[l - 1]) / (2.0 * (2 * l + 1));
+            Al[l] = v;
+            Bl[l] = -v;
         }
         if (a <= 0.5) {
-            B[0] = 1.0 - a;
-            A[0] = 1.0 - B[0];
+            Bl[0] = 1.0 - a;
+            Al[0] = 1.0 - Bl[0];
         } else {
-            A[0] = a;
-            B[0] = 1.0 - a;
+            Al[0] = a;
+            Bl[0] = 1.0 - a;
         }
     }
 }
 
+template <int KK>
+__device__ __forceinline__ void build_ab_t(double a, double* A, double* B, const GaussTab& gt)
+{
+    double xg[KK], wg[KK], Al[KK * KK], Bl[KK * KK];
+#pragma unroll
+    for (int g = 0; g < KK; ++g) {
+        xg[g] = gt.x[g];
+        wg[g] = gt.w[g];
+    }
+    build_ab_regs<KK>(a, xg, wg, Al, Bl);
+#pragma unroll
+    for (int j = 0; j < KK * KK; ++j) {
+        A[j] = Al[j];
+        B[j] = Bl[j];
+    }
+}
+
+__device__ __forceinline__ void build_ab(int k, double a, double* A, double* B, const GaussTab& gt)
+{
+    switch (k) {
+        case 1: build_ab_t<1>(a, A, B, gt); break;
+        case 2: build_ab_t<2>(a, A, B, gt); break;
+        case 3: build_ab_t<3>(a, A, B, gt); break;
+        case 4: build_ab_t<4>(a, A, B, gt); break;
+        case 5: build_ab_t<5>(a, A, B, gt); break;
+        case 6: build_ab_t<6>(a, A, B, gt); break;
+        case 7: build_ab_t<7>(a, A, B, gt); break;
+        default: build_ab_t<8>(a, A, B, gt); break;
+    }
+}
 
 }  // namespace sldg

@@ -128,6 +128,14 @@ struct Grid {
 // records msg as sldg_last_error() and returns st (sldg_abi.cu)
 sldg_status set_error(sldg_status st, const std::string& msg);
 
+// k-point Gauss-Legendre nodes (ascending) and weights on [-1, 1], computed once per k on the
+// host (Newton on P_k) and passed to the weight kernels by value (kernel-parameter bank).
+struct GaussTab {
+    double x[kMaxK];
+    double w[kMaxK];
+};
+const GaussTab& gauss_table(int k);
+
 // ---- kernel launchers (sldg_kernels.cu) -------------------------------------------------
 cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field, double shift,
                            int64_t n_entries, Weights& w, int* d_err, cudaStream_t s);
@@ -198,4 +206,8 @@ struct sldg_grid_s : public sldg::Grid {
     int64_t transposes = 0;        // sweeps that took the transpose path
     double* d_vnrec = nullptr;     // Gauss-node sweep: per-v-cell operator records
     int64_t vnrec_cap = 0;
+    // graph capture (sldg_graph_begin/end)
+    bool capturing = false, cap_profile = false;
+    int cap_cur = 0;
+    int64_t cap_launches = 0;
 };

@@ -39,22 +39,22 @@ __device__ __forceinline__ void store_slot(const Layout& L, const Arrays& a, int
 // form (reading R3), alpha == 0 -> A = 0, B = I and the exact-copy flag (reading R4).
 // ============================================================================================
 
-__global__ void build_weights_kernel(int k, int64_t nd, const double* __restrict__ field, double shift,
+template <int KK>
+__global__ void __launch_bounds__(32) build_weights_kernel(int64_t nd, const double* __restrict__ field, double shift,
                                      int64_t n_entries, int64_t* __restrict__ sh_raw,
                                      int64_t* __restrict__ sh_mod, int* __restrict__ cpy,
-                                     double* __restrict__ ab, double* __restrict__ rec, int* __restrict__ err)
+                                     double* __restrict__ ab, double* __restrict__ rec, int* __restrict__ err,
+                                     const GaussTab gt)
 {
-    int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_entries) return;
-    double nu = field ? field[e] : shift;
-    double* A = ab + e * 2 * k * k;
-    double* B = A + k * k;
+    const double nu = field ? field[e] : shift;
     int64_t is = 0;
     double a = 0.0;
     if (!(fabs(nu) < 4.611686018427387904e18)) {  // non-finite or |nu| >= 2^62
         atomicExch(err, 1);
     } else {
-        double fl = floor(nu);
+        const double fl = floor(nu);
         a = nu - fl;
         is = (int64_t)fl;
         if (a >= 1.0) {  // tiny negative nu: alpha rounds to 1 (reading R2)
@@ -62,29 +62,104 @@ __global__ void build_weights_kernel(int k, int64_t nd, const double* __restrict
             a = 0.0;
         }
     }
-    sh_raw[e] = is;
     int64_t m = is % nd;
-    sh_mod[e] = m < 0 ? m + nd : m;
-    cpy[e] = (a == 0.0);
-    for (int j = 0; j < k * k; ++j) {
-        A[j] = 0.0;
-        B[j] = ((j / k) == (j % k)) ? 1.0 : 0.0;
+    m = m < 0 ? m + nd : m;
+    const int cp = (a == 0.0);
+    // A, B in registers (alpha == 0: A = 0, B = I exactly, reading R4)
+    double A[KK * KK], B[KK * KK];
+    if (a != 0.0) {
+        double xg[KK], wg[KK];
+#pragma unroll
+        for (int g = 0; g < KK; ++g) {
+            xg[g] = gt.x[g];
+            wg[g] = gt.w[g];
+        }
+        build_ab_regs<KK>(a, xg, wg, A, B);
+    } else {
+#pragma unroll
+        for (int j = 0; j < KK * KK; ++j) {
+            A[j] = 0.0;
+            B[j] = ((j / KK) == (j % KK)) ? 1.0 : 0.0;
+        }
     }
-    if (a != 0.0) build_ab(k, a, A, B);
+    sh_raw[e] = is;
+    sh_mod[e] = m;
+    cpy[e] = cp;
+    double* pab = ab + e * 2 * KK * KK;
     // packed line record {A, B, i* mod n, copy} (16(k^2+1) bytes) for bulk copies into smem
-    double* r = rec + e * (2 * k * k + 2);
-    for (int j = 0; j < 2 * k * k; ++j) r[j] = A[j];
-    r[2 * k * k] = __longlong_as_double((long long)sh_mod[e]);
-    r[2 * k * k + 1] = __longlong_as_double((long long)cpy[e]);
+    double* r = rec + e * (2 * KK * KK + 2);
+#pragma unroll
+    for (int j = 0; j < KK * KK; ++j) {
+        pab[j] = A[j];
+        pab[KK * KK + j] = B[j];
+        r[j] = A[j];
+        r[KK * KK + j] = B[j];
+    }
+    r[2 * KK * KK] = __longlong_as_double((long long)m);
+    r[2 * KK * KK + 1] = __longlong_as_double((long long)cp);
+}
+
+const GaussTab& gauss_table(int k)
+{
+    static GaussTab tabs[kMaxK + 1];
+    static bool done[kMaxK + 1] = {};
+    if (!done[k]) {
+        GaussTab t{};
+        for (int i = 0; i < k; ++i) {  // Newton on P_k from the asymptotic guess of root i
+            double z = cos(3.141592653589793238462643 * (i + 0.75) / (k + 0.5)), dp = 1.0;
+            for (int it = 0; it < 100; ++it) {
+                double p0 = 1.0, p1 = z;
+                for (int m = 2; m <= k; ++m) {
+                    const double p2 = ((2 * m - 1) * z * p1 - (m - 1) * p0) / m;
+                    p0 = p1;
+                    p1 = p2;
+                }
+                const double pn = (k == 1) ? z : p1, pm1 = (k == 1) ? 1.0 : p0;
+                dp = k * (pm1 - z * pn) / (1.0 - z * z);
+                const double dz = pn / dp;
+                z -= dz;
+                if (fabs(dz) < 1e-17) break;
+            }
+            double p0 = 1.0, p1 = z;  // derivative at the converged root
+            for (int m = 2; m <= k; ++m) {
+                const double p2 = ((2 * m - 1) * z * p1 - (m - 1) * p0) / m;
+                p0 = p1;
+                p1 = p2;
+            }
+            const double pn = (k == 1) ? z : p1, pm1 = (k == 1) ? 1.0 : p0;
+            dp = k * (pm1 - z * pn) / (1.0 - z * z);
+            t.x[k - 1 - i] = z;  // i = 0 is the largest root: ascending order
+            t.w[k - 1 - i] = 2.0 / ((1.0 - z * z) * dp * dp);
+        }
+        if (k & 1) t.x[k / 2] = 0.0;
+        tabs[k] = t;
+        done[k] = true;
+    }
+    return tabs[k];
 }
 
 cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field, double shift,
                            int64_t n_entries, Weights& w, int* d_err, cudaStream_t s)
 {
-    int threads = 128;
+    // small blocks: one entry per thread is a serial fp64 build, so spread entries over SMs
+    int threads = 32;
     int64_t blocks = (n_entries + threads - 1) / threads;
-    build_weights_kernel<<<(unsigned)blocks, threads, 0, s>>>(lay.k, nd, d_field, shift, n_entries,
-                                                              w.shift, w.smod, w.copy, w.ab, w.rec, d_err);
+    const GaussTab& gt = gauss_table(lay.k);
+#define SLDG_W(KK)                                                                                           \
+    build_weights_kernel<KK><<<(unsigned)blocks, threads, 0, s>>>(nd, d_field, shift, n_entries, w.shift, w.smod, \
+                                                                  w.copy, w.ab, w.rec, d_err, gt)
+    switch (lay.k) {
+        case 1: SLDG_W(1); break;
+        case 2: SLDG_W(2); break;
+        case 3: SLDG_W(3); break;
+        case 4: SLDG_W(4); break;
+        case 5: SLDG_W(5); break;
+        case 6: SLDG_W(6); break;
+        case 7: SLDG_W(7); break;
+        case 8: SLDG_W(8); break;
+        default: return cudaErrorInvalidValue;
+    }
+#undef SLDG_W
     return cudaGetLastError();
 }
 

@@ -293,15 +293,13 @@ __global__ void vp_x_field_kernel(int64_t nv, double lo_v, double h_v, double ta
 
 // V7 (NEXT-3): nu[i * k + n] = (lo_v + (i + 1/2) h_v + xi_n h_v / 2) * tau / h_x at the Gauss nodes
 __global__ void vp_x_nodal_field_kernel(int64_t nv, int k, double lo_v, double h_v, double tau, double h_x,
-                                        double* nu)
+                                        double* nu, const GaussTab gt)
 {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= nv * k) return;
-    double xg[kMaxK], wg[kMaxK];
-    dev_gauss(k, xg, wg);
     const int64_t i = t / k;
     const int n = (int)(t - i * k);
-    nu[t] = (lo_v + ((double)i + 0.5) * h_v + xg[n] * h_v / 2) * tau / h_x;
+    nu[t] = (lo_v + ((double)i + 0.5) * h_v + gt.x[n] * h_v / 2) * tau / h_x;
 }
 
 // V5: nu[i_x] = E_c(i_x) * tau / h_v
@@ -440,7 +438,8 @@ sldg_status vp_x_sweeps(sldg_vp vp, double tau)
         sldg_status st;
         if (vp->nodal) {
             vp_x_nodal_field_kernel<<<nblk(nv * vp->k), 256, 0, g->stream>>>(nv, vp->k, g->lo[dv], g->h[dv], tau,
-                                                                             g->h[c], vp->d_nux[c]);
+                                                                             g->h[c], vp->d_nux[c],
+                                                                             gauss_table(vp->k));
             VCU(cudaGetLastError());
             g->launches += 1;
             st = sldg_advect_vnodes_device(g, c, dv, vp->d_nux[c]);

@@ -30,7 +30,7 @@ namespace {
 __host__ __device__ __forceinline__ int64_t vn_rec_words(int k) { return 2 + (int64_t)kVnMaxOfs * k * k * k * k; }
 
 __global__ void vnode_weights_kernel(int k, const double* __restrict__ nodal, int64_t nv, double* __restrict__ rec,
-                                     int* __restrict__ err)
+                                     int* __restrict__ err, const GaussTab gt)
 {
     const int64_t j = blockIdx.x;
     if (j >= nv) return;
@@ -41,8 +41,9 @@ __global__ void vnode_weights_kernel(int k, const double* __restrict__ nodal, in
     __shared__ int s_nofs, s_bad;
     double* r = rec + j * vn_rec_words(k);
     if (threadIdx.x == 0) {
-        double xg[kMaxK], wg[kMaxK], P[kMaxK + 2];
-        dev_gauss(k, xg, wg);
+        double P[kMaxK + 2];
+        const double* xg = gt.x;
+        const double* wg = gt.w;
         for (int n = 0; n < k; ++n) {
             dev_legendre(k - 1, xg[n], P);
             for (int m = 0; m < k; ++m) {
@@ -71,7 +72,7 @@ __global__ void vnode_weights_kernel(int k, const double* __restrict__ nodal, in
                     is += 1;
                     a = 0.0;
                 }
-                if (a != 0.0) build_ab(k, a, A, B);
+                if (a != 0.0) build_ab(k, a, A, B, gt);
             }
             sI[n] = is;
             omin = is < omin ? is : omin;
@@ -202,7 +203,7 @@ int64_t vnode_rec_words(int k) { return vn_rec_words(k); }
 
 cudaError_t launch_vnode_weights(int k, const double* d_nodal, int64_t nv, double* d_rec, int* d_err, cudaStream_t s)
 {
-    vnode_weights_kernel<<<(unsigned)nv, 128, 0, s>>>(k, d_nodal, nv, d_rec, d_err);
+    vnode_weights_kernel<<<(unsigned)nv, 128, 0, s>>>(k, d_nodal, nv, d_rec, d_err, gauss_table(k));
     return cudaGetLastError();
 }
 

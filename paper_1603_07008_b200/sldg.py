@@ -29,7 +29,8 @@ EXPORTS = [
     "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_halo_plan", "sldg_layer_owner",
     "sldg_sweep_kernel", "sldg_vp_create", "sldg_vp_destroy", "sldg_vp_density", "sldg_vp_field",
     "sldg_vp_step", "sldg_transpose_plan", "sldg_transpose_count", "sldg_advect_vnodes",
-    "sldg_advect_vnodes_device", "sldg_vp_set_nodal",
+    "sldg_advect_vnodes_device", "sldg_vp_set_nodal", "sldg_graph_begin", "sldg_graph_end",
+    "sldg_graph_launch", "sldg_graph_destroy",
 ]
 
 
@@ -102,6 +103,10 @@ def lib():
         "sldg_vp_field": [vp, dp, dp, dp, dp],
         "sldg_vp_step": [vp, ctypes.c_double, dp],
         "sldg_vp_set_nodal": [vp, ctypes.c_int],
+        "sldg_graph_begin": [vp],
+        "sldg_graph_end": [vp, ctypes.POINTER(vp)],
+        "sldg_graph_launch": [vp],
+        "sldg_graph_destroy": [vp],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -301,6 +306,17 @@ class Grid:
     def launch_count(self) -> int:
         return int(lib().sldg_launch_count(self.h))
 
+    def graph_begin(self):
+        """Start capturing asynchronous calls into a CUDA graph (sldg_graph_begin)."""
+        _check(lib().sldg_graph_begin(self.h))
+
+    def graph_end(self) -> "Graph":
+        h = ctypes.c_void_p()
+        _check(lib().sldg_graph_end(self.h, ctypes.byref(h)))
+        gr = Graph(h)
+        self._dependents.add(gr)
+        return gr
+
     def transpose_count(self) -> int:
         n = ctypes.c_int64()
         _check(lib().sldg_transpose_count(self.h, ctypes.byref(n)))
@@ -368,3 +384,24 @@ class VlasovPoisson:
             return float(w[0])
         _check(lib().sldg_vp_step(self.h, float(dt), None))
         return None
+
+
+class Graph:
+    """A captured sequence of asynchronous grid calls (sldg_graph_*)."""
+
+    def __init__(self, h):
+        self.h = h
+
+    def launch(self):
+        _check(lib().sldg_graph_launch(self.h))
+
+    def destroy(self):
+        if self.h:
+            lib().sldg_graph_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
