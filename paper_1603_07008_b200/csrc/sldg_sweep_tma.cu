@@ -943,6 +943,13 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
     if (const char* e = getenv("SLDG_TMA_W")) Wmax = atoi(e);        // tuning overrides
     if (const char* e = getenv("SLDG_TMA_TSUB")) Tsub0 = atoi(e);
     if (const char* e = getenv("SLDG_TMA_SDIV")) sdiv = atoi(e);
+    // Widest tile first.  A grid short of tiles (< 4 per SM at that width, e.g. C2's 1024-layer v
+    // sweep) takes W = 64 instead: more column tiles AND a stage row 4x narrower, so Tsub reaches
+    // its cap (measured on C2: 1.71 -> 2.04 TB/s; W = 32 is slower, profiles/round1/tuning.md).
+    int64_t perp = outer ? 1 : lay.layers;  // tiles along the dims other than lo and d
+    if (!outer)
+        for (int e = sw.dim + 1; e < lay.D - 1; ++e) perp *= lay.n[e];
+    const int64_t nline_p = outer ? lay.layers : sw.nd;
     for (int w : {256, 128, 64, 32}) {
         if (M_lo % w != 0 || w > Wmax) continue;
         int ts = (int)std::min<int64_t>(Tsub0, budget / sdiv / ((int64_t)w * bpc_max) - 4);
@@ -950,6 +957,14 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
         W = w;
         Tsub = ts;
         break;
+    }
+    if (W > 64 && M_lo % 64 == 0 && !getenv("SLDG_TMA_W")) {
+        const int64_t tiles = (M_lo / W) * perp * ((nline_p + Tsub - 1) / Tsub);
+        const int ts64 = (int)std::min<int64_t>(Tsub0, budget / sdiv / (64LL * bpc_max) - 4);
+        if (tiles < 4LL * g_num_sms * ctas && ts64 >= 4) {
+            W = 64;
+            Tsub = ts64;
+        }
     }
     if (W == 0) return false;
     const int Rmax = Tsub + 4;
