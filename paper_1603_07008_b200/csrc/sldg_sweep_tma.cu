@@ -883,7 +883,15 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
     // registers per thread -- twice the warps to hide latency, at the cost of spills)
     // Measured: k <= 2 fits 96 registers without hurtful spills and gains from the extra warps
     // (C4 64^4 k=2: 375 -> 467 GDoF/s); k = 3 loses (C5: 693 -> 643 GDoF/s).
+    // Per sweep kind (C4 64^4 k = 2, profiles/round1/tuning.md): the d = 0 sweep and strided
+    // sweeps over fewer than 256 cells below d gain from 2 CTAs (d0 3.8 vs 2.7 TB/s), strided
+    // sweeps with full 256-column rows from 1 CTA with twice the stage (4.9 / 5.3 vs 4.5 / 4.8).
     int ctas = (k <= 2) ? 2 : 1;
+    if (k <= 2 && sw.dim > 0) {
+        int64_t mlo = 1;
+        for (int e = 0; e < ((sw.dim == lay.D - 1) ? lay.D - 1 : sw.dim); ++e) mlo *= lay.n[e];
+        if (mlo % 256 == 0) ctas = 1;
+    }
     if (const char* e = getenv("SLDG_TMA_CTAS")) ctas = (atoi(e) == 2) ? 2 : 1;
     const int64_t budget = std::min<int64_t>(g_smem_optin, 200 * 1024) / ctas - 256 - (ctas - 1) * 1024;
     const int bpc_max = (lay.prec == SLDG_FP64) ? 8 * k : 8 + 4 * (k - 1);  // bytes per column, mass group
@@ -904,7 +912,7 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
         const int64_t cs = R * n0;
         const int64_t group_bytes = cs * bpc_max;  // one coupled group of the tile, worst case
         const int G = lay.K / k;
-        int64_t d0div = 3;  // stage <= budget / d0div (tuning override SLDG_TMA_D0DIV)
+        int64_t d0div = (k <= 2) ? 2 : 3;  // stage <= budget / d0div (C4: 2 beats 3, 3.8 -> 4.1 TB/s; override SLDG_TMA_D0DIV)
         if (const char* e = getenv("SLDG_TMA_D0DIV")) d0div = atoi(e);
         const int64_t target = budget / d0div;
         if (group_bytes > budget / 2) return false;
