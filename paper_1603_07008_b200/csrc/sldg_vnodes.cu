@@ -127,22 +127,42 @@ template <int KK>
 __global__ void __launch_bounds__(256) vnode_sweep_kernel(Layout lay, int d, int e, const double* __restrict__ rec,
                                                          Arrays src, Arrays dst)
 {
+    constexpr int K2 = KK * KK, K4 = K2 * K2;
+    constexpr int RS = (K2 + 1) & ~1;  // shared-memory row stride (even: 16-byte row pairs)
+    extern __shared__ __align__(16) double sM[];  // [kVnMaxOfs][K2][RS]
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (t >= lay.cells) return;
+    const bool valid = t < lay.cells;
     const int D = lay.D;
-    const int64_t layer = t / lay.L, inner = t - layer * lay.L;
+    const int64_t tt = valid ? t : blockIdx.x * (int64_t)blockDim.x;
+    const int64_t layer = tt / lay.L, inner = tt - layer * lay.L;
     const int64_t lp = lay.pad + layer;
     // index along d and along e (global)
-    auto idx_of = [&](int dd) -> int64_t {
-        if (dd == D - 1) return lay.first_layer + layer;
-        return (inner / lay.S[dd]) % lay.n[dd];
+    auto idx_of = [&](int dd, int64_t lay_, int64_t in_) -> int64_t {
+        if (dd == D - 1) return lay.first_layer + lay_;
+        return (in_ / lay.S[dd]) % lay.n[dd];
     };
-    const int64_t id = idx_of(d), j = idx_of(e);
+    const int64_t id = idx_of(d, layer, inner), j = idx_of(e, layer, inner);
+    // the CTA's cells usually share their v-cell (C5: 256 consecutive cells along x1 or x2);
+    // then its operators are staged in shared memory once and read as 16-byte broadcasts
+    const int64_t t0 = blockIdx.x * (int64_t)blockDim.x;
+    const int64_t l0 = t0 / lay.L;
+    const int64_t j0 = idx_of(e, l0, t0 - l0 * lay.L);
+    const bool uni = __syncthreads_and(!valid || j == j0);
     const double* r = rec + j * vn_rec_words(KK);
     const int64_t omin = (int64_t)__double_as_longlong(__ldg(&r[0]));
     const int nofs = (int)__double_as_longlong(__ldg(&r[1]));
+    if (uni) {
+        const double* M0 = rec + j0 * vn_rec_words(KK) + 2;
+        for (int x = threadIdx.x; x < kVnMaxOfs * K4; x += blockDim.x) {
+            const int o = x / K4, rem = x - o * K4, m = rem / K2, l = rem - m * K2;
+            sM[(o * K2 + m) * RS + l] = __ldg(&M0[x]);
+        }
+        if (RS != K2)
+            for (int x = threadIdx.x; x < kVnMaxOfs * K2; x += blockDim.x) sM[x * RS + K2] = 0.0;
+        __syncthreads();
+    }
+    if (!valid) return;
     const double* M = r + 2;
-    constexpr int K2 = KK * KK, K4 = K2 * K2;
     // source positions per offset
     int64_t s_lp[kVnMaxOfs], s_in[kVnMaxOfs];
     const int64_t nd = lay.n[d];
@@ -161,6 +181,21 @@ __global__ void __launch_bounds__(256) vnode_sweep_kernel(Layout lay, int d, int
     int kd = 1, ke = 1;
     for (int x = 0; x < d; ++x) kd *= KK;
     for (int x = 0; x < e; ++x) ke *= KK;
+    // element offsets of the block's k^2 slots from its first slot, in planes of L cells
+    int64_t loff[K2];
+#pragma unroll
+    for (int le = 0; le < KK; ++le)
+#pragma unroll
+        for (int ld = 0; ld < KK; ++ld) loff[le * KK + ld] = (int64_t)(ld * kd + le * ke) * lay.L;
+    // per source offset: slot-q pointers are fb[o] + q L (fp32 slots) and db[o] + q L (fp64 slots)
+    const float* fb[kVnMaxOfs];
+    const double* db[kVnMaxOfs];
+    const int nd_ = lay.nd, nf_ = lay.K - lay.nd;
+#pragma unroll
+    for (int o = 0; o < kVnMaxOfs; ++o) {
+        fb[o] = src.pl + (s_lp[o] * nf_ - nd_) * lay.L + s_in[o];
+        db[o] = src.mass + s_lp[o] * nd_ * lay.L + s_in[o];
+    }
     const int nblk = lay.K / K2;
     for (int b = 0; b < nblk; ++b) {
         // slot base of block b: the other dims' indices (all but d, e) from b
@@ -172,28 +207,62 @@ __global__ void __launch_bounds__(256) vnode_sweep_kernel(Layout lay, int d, int
             }
             kp *= KK;
         }
+        const int64_t q0L = (int64_t)q0 * lay.L;
+        // the block's slots are all fp32 unless it holds an fp64 slot (q < nd)
+        const bool all_f = (q0 >= nd_);
         double out[K2];
 #pragma unroll
         for (int m = 0; m < K2; ++m) out[m] = 0.0;
         for (int o = 0; o < nofs; ++o) {
-            double v[K2];
+            double v[RS];
+            if (all_f) {
+                const float* p = fb[o] + q0L;
 #pragma unroll
-            for (int le = 0; le < KK; ++le)
+                for (int i = 0; i < K2; ++i) v[i] = (double)p[loff[i]];
+            } else {
 #pragma unroll
-                for (int ld = 0; ld < KK; ++ld) v[le * KK + ld] = vn_load(lay, src, q0 + ld * kd + le * ke, s_lp[o], s_in[o]);
-            const double* Mo = M + o * K4;
+                for (int le = 0; le < KK; ++le)
 #pragma unroll
-            for (int m = 0; m < K2; ++m) {
-                double acc = out[m];
+                    for (int ld = 0; ld < KK; ++ld)
+                        v[le * KK + ld] = vn_load(lay, src, q0 + ld * kd + le * ke, s_lp[o], s_in[o]);
+            }
+            if (RS != K2) v[K2] = 0.0;
+            if (uni) {
+                const double* Mo = sM + o * K2 * RS;
 #pragma unroll
-                for (int l = 0; l < K2; ++l) acc = fma(__ldg(&Mo[m * K2 + l]), v[l], acc);
-                out[m] = acc;
+                for (int m = 0; m < K2; ++m) {
+                    double acc = out[m];
+#pragma unroll
+                    for (int l = 0; l < RS; l += 2) {
+                        const double2 mm = *(const double2*)&Mo[m * RS + l];
+                        acc = fma(mm.x, v[l], acc);
+                        if (l + 1 < K2) acc = fma(mm.y, v[l + 1], acc);
+                    }
+                    out[m] = acc;
+                }
+            } else {
+                const double* Mo = M + o * K4;
+#pragma unroll
+                for (int m = 0; m < K2; ++m) {
+                    double acc = out[m];
+#pragma unroll
+                    for (int l = 0; l < K2; ++l) acc = fma(__ldg(&Mo[m * K2 + l]), v[l], acc);
+                    out[m] = acc;
+                }
             }
         }
+        if (all_f) {
+            float* p = dst.pl + (lp * nf_ - nd_) * lay.L + inner + q0L;
 #pragma unroll
-        for (int me = 0; me < KK; ++me)
+            for (int me = 0; me < KK; ++me)
 #pragma unroll
-            for (int md = 0; md < KK; ++md) vn_store(lay, dst, q0 + md * kd + me * ke, lp, inner, out[me * KK + md]);
+                for (int md = 0; md < KK; ++md) p[loff[me * KK + md]] = __double2float_rn(out[me * KK + md]);
+        } else {
+#pragma unroll
+            for (int me = 0; me < KK; ++me)
+#pragma unroll
+                for (int md = 0; md < KK; ++md) vn_store(lay, dst, q0 + md * kd + me * ke, lp, inner, out[me * KK + md]);
+        }
     }
 }
 
@@ -212,11 +281,13 @@ cudaError_t launch_vnode_sweep(const Layout& lay, int d, int e, const double* d_
 {
     const unsigned blocks = (unsigned)((lay.cells + 255) / 256);
     if (blocks == 0) return cudaSuccess;
+    const int k2 = lay.k * lay.k;
+    const size_t smem = (size_t)kVnMaxOfs * k2 * ((k2 + 1) & ~1) * sizeof(double);
     switch (lay.k) {
-        case 1: vnode_sweep_kernel<1><<<blocks, 256, 0, s>>>(lay, d, e, d_rec, src, dst); break;
-        case 2: vnode_sweep_kernel<2><<<blocks, 256, 0, s>>>(lay, d, e, d_rec, src, dst); break;
-        case 3: vnode_sweep_kernel<3><<<blocks, 256, 0, s>>>(lay, d, e, d_rec, src, dst); break;
-        case 4: vnode_sweep_kernel<4><<<blocks, 256, 0, s>>>(lay, d, e, d_rec, src, dst); break;
+        case 1: vnode_sweep_kernel<1><<<blocks, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
+        case 2: vnode_sweep_kernel<2><<<blocks, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
+        case 3: vnode_sweep_kernel<3><<<blocks, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
+        case 4: vnode_sweep_kernel<4><<<blocks, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
