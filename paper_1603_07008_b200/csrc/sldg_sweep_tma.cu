@@ -873,7 +873,19 @@ static bool make_tmap(CUtensorMap* tm, bool f64, void* base, const int64_t* dims
 }
 
 // Returns true and fills `pl` when the TMA path applies to this sweep.
+static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int force_ctas);
+
 bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
+{
+    *pl = TmaPlan{};
+    if (tma_plan_ctas(lay, sw, pl, 0)) return true;
+    // a k <= 2 plan with 2 CTAs per SM halves the shared memory per CTA; a stage that no longer
+    // fits twice (e.g. a 4096-cell line of the mass group) still fits with one CTA
+    if (pl->ctas == 2 && !getenv("SLDG_TMA_CTAS")) return tma_plan_ctas(lay, sw, pl, 1);
+    return false;
+}
+
+static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int force_ctas)
 {
     query_device();
     if (!encoder()) return false;
@@ -893,6 +905,7 @@ bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl)
         if (mlo % 256 == 0) ctas = 1;
     }
     if (const char* e = getenv("SLDG_TMA_CTAS")) ctas = (atoi(e) == 2) ? 2 : 1;
+    if (force_ctas) ctas = force_ctas;
     const int64_t budget = std::min<int64_t>(g_smem_optin, 200 * 1024) / ctas - 256 - (ctas - 1) * 1024;
     const int bpc_max = (lay.prec == SLDG_FP64) ? 8 * k : 8 + 4 * (k - 1);  // bytes per column, mass group
     const int NT = kTmaConsumerWarps * 32;
