@@ -204,7 +204,7 @@ def main():
     ap.add_argument("--k", type=int, default=None)
     ap.add_argument("--eps", type=float, default=0.01)
     ap.add_argument("--ref-lines", type=int, default=4096)
-    ap.add_argument("--cpu-lines", type=int, default=25000)
+    ap.add_argument("--cpu-lines", type=int, default=45000)  # ~15 s of oracle time on the GPU box
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--compare-fp64", action=argparse.BooleanOptionalAction, default=True,
