@@ -3,7 +3,6 @@ inputs.  Tolerances (BASELINE.json north_star): fp64 mass slot |d| <
 max|c0| per array; fp32 slots |d| <= 8 ulp_fp32(max|plane|) per plane; fp64 variant 1e-13 *
 max|plane| per plane; integer shifts bit-exact; mass 1e-13 relative.
 """
-import itertools
 
 import numpy as np
 import pytest
@@ -392,7 +391,6 @@ def test_forced_halo_path_matches_oracle(dims, k, precision, nccl_self):
     split) run on one GPU: SLDG_DIST_FORCE_HALO makes the rank its own ring neighbour.  Every
     dim is swept (pad > 0 changes every kernel's addressing); the layer-dim sweeps use shifts
     up to the halo width and a per-lane field."""
-    from paper_1603_07008_b200 import SldgError
     D, K = len(dims), k ** len(dims)
     c = sldg_inputs.random_coeffs(dims, k, 4242)
     ref_in = oracle_input(c, K, precision)
