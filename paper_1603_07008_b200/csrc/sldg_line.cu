@@ -40,10 +40,10 @@ __device__ __forceinline__ void l_wait(uint64_t* bar, uint32_t parity)
         "{\n"
         ".reg .pred p;\n"
         "LWAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra LWAIT_%=;\n"
         "}\n" ::"r"(l_smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)  // suspend-time hint (ns)
         : "memory");
 }
 __device__ __forceinline__ void l_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar)

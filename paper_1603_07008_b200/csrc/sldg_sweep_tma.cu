@@ -67,10 +67,10 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
         "{\n"
         ".reg .pred p;\n"
         "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
         "@!p bra WAIT_%=;\n"
         "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
+        "r"(parity), "r"(1000000u)  // suspend-time hint (ns): sleep until the phase completes
         : "memory");
 }
 // 1D bulk copy global -> shared (fallback for rows that wrap around a periodic line)
