@@ -322,18 +322,20 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
         return tfield_index(sw, idx, D);
     };
     // The shifts of the NEXT tile's columns (for its shift span) are loaded while the current
-    // tile streams (software prefetch).
-    int64_t pf_sh[8];
+    // tile streams (software prefetch) -- in the 1-CTA-per-SM instance; the 2-CTA instance (96
+    // registers) loads them at the tile start instead of holding 8 of them across the tile.
+    constexpr bool PF = (MINB == 1);
+    int64_t pf_sh[PF ? 8 : 1];
     auto prefetch = [&](int64_t tl) {
         int64_t cb, hi, layer, t0;
         decode(tl, cb, hi, layer, t0);
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
+        for (int i = 0; i < (PF ? 8 : 1); ++i) {
             const int cc = lane + 32 * i;
             pf_sh[i] = (cc < W) ? __ldg(&sw.shift[findex(cb * W + cc, hi, layer)]) : 0;
         }
     };
-    if ((int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x);
+    if (PF && (int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x);
 
     uint32_t it = 0;  // stage-use counter, identical in every warp
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
@@ -344,11 +346,20 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
         const int64_t inner_base = outer ? cb * W : cb * W + hi * M_lo * sw.nd;  // column 0, coordinate 0
 
         int64_t imin = INT64_MAX, imax = INT64_MIN;
+        if (PF) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            if (lane + 32 * i < W) {
-                imin = pf_sh[i] < imin ? pf_sh[i] : imin;
-                imax = pf_sh[i] > imax ? pf_sh[i] : imax;
+            for (int i = 0; i < (PF ? 8 : 1); ++i) {
+                if (lane + 32 * i < W) {
+                    imin = pf_sh[i] < imin ? pf_sh[i] : imin;
+                    imax = pf_sh[i] > imax ? pf_sh[i] : imax;
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (int cc = lane; cc < W; cc += 32) {
+                const int64_t sh = __ldg(&sw.shift[findex(cb * W + cc, hi, layer)]);
+                imin = sh < imin ? sh : imin;
+                imax = sh > imax ? sh : imax;
             }
         }
 #pragma unroll
@@ -357,7 +368,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
             imin = a < imin ? a : imin;
             imax = b > imax ? b : imax;
         }
-        if (tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
+        if (PF && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
         const int64_t span = imax - imin;
         // sub-chunks of te targets: rows = te + 1 + span <= Rmax, balanced over the tile
         const int tmax = (int)(Rmax - 1 - span);
