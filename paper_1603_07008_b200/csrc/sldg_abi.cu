@@ -744,6 +744,9 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
         K *= k;
     }
     if (K > (1 << 20)) return fail(SLDG_EINVAL, "k^D too large");
+    // k^D == 1: the only coefficient is the mass, stored fp64 either way -- the mixed layout is
+    // the fp64 layout (one fp64 plane, no fp32 planes), and the kernels treat it as such
+    if (K == 1 && prec == SLDG_MIXED) prec = SLDG_FP64;
     int rank = 0, world = 1;
     if (dist) {
         rank = dist->rank;
