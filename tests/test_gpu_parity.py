@@ -549,3 +549,48 @@ def test_randomized_shapes_match_oracle(seed):
         assert_parity(g.get_coeffs(), ref, K, precision, f"seed={seed} dims={dims} k={k} dim={dim} "
                       f"kernel={g.sweep_kernel(dim)}", ref_in, dim, k)
     g.destroy()
+
+
+@pytest.mark.parametrize("seed", list(range(32)))
+def test_randomized_sharded_paths_match_oracle(seed):
+    """Random 2-5D grids on the single-GPU stand-ins of the multi-GPU paths: forced halo layers
+    (random max_halo), forced transposes, NCCL self-transfers; sweeps along the layer dim with
+    shifts that fit the halo, exceed it (automatic transpose), or are per-line fields over the
+    slab dim; plus a sweep along another dim."""
+    rng = np.random.default_rng(5000 + seed)
+    D = int(rng.integers(2, 6))
+    k = int(rng.integers(1, 5))
+    dims = [int(rng.choice([1, 2, 3, 4, 5, 8, 12, 16, 32, 64])) for _ in range(D)]
+    dims[-1] = int(rng.integers(2, 20))
+    while np.prod(dims) * k ** D > 1_000_000:
+        i = int(np.argmax(dims[:-1]))
+        dims[i] = max(1, dims[i] // 2)
+    precision = ["mixed", "fp64"][int(rng.integers(0, 2))]
+    mode = int(rng.integers(0, 3))
+    kw = dict(max_halo=int(rng.integers(1, 4)), nccl_self=bool(rng.random() < 0.4))
+    if mode == 0:
+        kw["force_halo"] = True
+    elif mode == 1:
+        kw["force_transpose"] = True
+    else:
+        kw["force_halo"] = True
+        kw["force_transpose"] = True
+    K = k ** D
+    c = sldg_inputs.random_coeffs(dims, k, seed)
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision, **kw)
+    n = dims[-1]
+    cases = [(D - 1, float(rng.uniform(-1.5, 1.5)), None, 0),
+             (D - 1, float(rng.uniform(-3 * n, 3 * n)), None, 0)]
+    mask = (1 << (D - 2)) | (1 if rng.random() < 0.5 else 0)
+    nf = int(np.prod([dims[e] for e in range(D) if mask >> e & 1]))
+    cases.append((D - 1, 0.0, rng.uniform(-2.2 * n, 2.2 * n, nf), mask))
+    cases.append((int(rng.integers(0, D - 1)), float(rng.uniform(-5, 5)), None, 0))
+    for dim, shift, field, fm in cases:
+        g.set_coeffs(c)
+        g.advect(dim, shift=shift, field=field, field_mask=fm)
+        ref = oracle.advect(ref_in, dims, k, dim, shift=shift, field=field, field_mask=fm,
+                            n_double=n_double(precision, K))
+        assert_parity(g.get_coeffs(), ref, K, precision,
+                      f"seed={seed} dims={dims} k={k} dim={dim} nu={shift} kw={kw}", ref_in, dim, k)
+    g.destroy()
