@@ -125,3 +125,26 @@ def test_general_layout_rejected_in_multid():
     g = _Grid([8, 8], 2, precision=4)  # == fp64
     assert g.memory_bytes() == 64 * 8 * 4
     g.destroy()
+
+
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_randomized_lines_all_layouts(seed):
+    """Random 1D lines (N from 1 to 70000, with and without N % 4 == 0), random k and number of
+    fp64 slots, random shifts: the line kernels against the oracle."""
+    rng = np.random.default_rng(300 + seed)
+    N = int(rng.choice([1, 2, 3, 5, 17, 63, 1024, 1028, 1030, 4099, 8192, 65536, 69996]))
+    k = int(rng.integers(1, 5))
+    nd = int(rng.integers(0, k + 1))
+    c = sldg_inputs.random_coeffs([N], k, seed)
+    src = oracle.round_layout(c, k, nd)
+    g = _Grid([N], k, precision=nd)
+    for nu in [float(rng.uniform(-3 * N, 3 * N)), float(rng.uniform(-1, 1)), float(rng.integers(-N, N))]:
+        g.set_coeffs(c)
+        g.advect(0, shift=nu)
+        got = g.get_coeffs()
+        ref = oracle.advect(src, [N], k, 0, shift=nu, n_double=nd)
+        if nu == round(nu):
+            assert got.tobytes() == ref.tobytes()
+        else:
+            _parity(got, ref, k, nd, src)
+    g.destroy()

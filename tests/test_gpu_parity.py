@@ -594,3 +594,42 @@ def test_randomized_sharded_paths_match_oracle(seed):
         assert_parity(g.get_coeffs(), ref, K, precision,
                       f"seed={seed} dims={dims} k={k} dim={dim} nu={shift} kw={kw}", ref_in, dim, k)
     g.destroy()
+
+
+@pytest.mark.parametrize("seed", list(range(16)))
+def test_randomized_medium_grids_match_oracle(seed):
+    """Random 2-4D grids of up to ~8M DoF (TMA plan branches: W selection and the W = 64 rule,
+    1- and 2-CTA instances, partial d = 0 tiles, R lines per tile, sub-chunk splits) -- every dim
+    swept once against the oracle."""
+    rng = np.random.default_rng(9000 + seed)
+    D = int(rng.integers(2, 5))
+    k = int(rng.integers(1, 5))
+    dims = [int(rng.choice([4, 8, 12, 16, 20, 24, 28, 32, 36, 40, 48, 60, 64, 100, 128, 132, 192, 256, 260,
+                            512, 1024, 1028, 2048]))
+            for _ in range(D)]
+    while np.prod(dims) * k ** D > 8_000_000:
+        i = int(np.argmax(dims))
+        dims[i] = max(4, (dims[i] // 2) // 4 * 4)
+    precision = ["mixed", "fp64"][int(rng.integers(0, 2))]
+    K = k ** D
+    c = sldg_inputs.random_coeffs(dims, k, seed)
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision)
+    for dim in range(D):
+        others = [e for e in range(D) if e != dim]
+        mask = 0
+        for e in others:
+            if rng.random() < 0.5:
+                mask |= 1 << e
+        if mask:
+            nf = int(np.prod([dims[e] for e in range(D) if mask >> e & 1]))
+            field, shift = rng.uniform(-4.5, 4.5, nf), 0.0
+        else:
+            field, shift = None, float(rng.uniform(-40, 40))
+        g.set_coeffs(c)
+        g.advect(dim, shift=shift, field=field, field_mask=mask)
+        ref = oracle.advect(ref_in, dims, k, dim, shift=shift, field=field, field_mask=mask,
+                            n_double=n_double(precision, K))
+        assert_parity(g.get_coeffs(), ref, K, precision,
+                      f"seed={seed} dims={dims} k={k} dim={dim} kernel={g.sweep_kernel(dim)}", ref_in, dim, k)
+    g.destroy()
