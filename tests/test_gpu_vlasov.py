@@ -193,3 +193,42 @@ def test_vp_rejects_bad_grids():
     with pytest.raises(SldgError):
         VlasovPoisson(g, 1)
     g.destroy()
+
+
+@pytest.mark.parametrize("seed", list(range(8)))
+def test_randomized_strang_steps(seed):
+    """Random 1+1D / 2+2D / 3+3D grids, k, storage, nodal or cell-centre x sweeps, forced halo:
+    one Strang step against the oracle."""
+    from paper_1603_07008_b200 import Grid, VlasovPoisson
+    rng = np.random.default_rng(800 + seed)
+    dx = int(rng.integers(1, 4))
+    k = int(rng.integers(1, 4)) if dx < 3 else 2
+    nx = [int(rng.choice([4, 6, 8, 12, 16])) for _ in range(dx)]
+    nv = [int(rng.choice([4, 8, 10, 16])) for _ in range(dx)]
+    dims = nx + nv
+    precision = ["mixed", "fp64"][int(rng.integers(0, 2))]
+    nodal = bool(rng.random() < 0.5)
+    kw = dict(force_halo=True, max_halo=2) if rng.random() < 0.3 else {}
+    lo = [0.0] * dx + [-6.0] * dx
+    hi = [4 * np.pi] * dx + [6.0] * dx
+    g = Grid(dims, k, lo=lo, hi=hi, precision=precision, **kw)
+    vp = VlasovPoisson(g, dx)
+    if nodal:
+        vp.set_nodal(True)
+    K = k ** (2 * dx)
+    nd = 1 if (precision == "mixed" and K > 1) else K
+    kinds = ["x"] * dx + ["v"] * dx
+    c = sldg_inputs.assemble_separable(sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=0.3), dims, k)
+    g.set_coeffs(c)
+    cur = g.get_coeffs()
+    w = vp.step(0.3, energy=True)
+    ref, _, wref = ovp.strang_step(cur, dims, k, dx, lo, hi, 0.3, n_double=nd, nodal=nodal)
+    assert abs(w - wref) <= 1e-12 * max(wref, 1e-300)
+    got = g.get_coeffs()
+    for q in range(K):
+        m = np.max(np.abs(ref[:, q]))
+        d = np.max(np.abs(got[:, q] - ref[:, q]))
+        tol = 1e-13 * max(np.max(np.abs(ref)), 1e-300) if q < nd else 8.0 * float(np.spacing(np.float32(m))) + 1e-30
+        assert d <= tol, (seed, q, d, tol)
+    vp.destroy()
+    g.destroy()

@@ -105,3 +105,32 @@ def test_vnodes_free_streaming_beats_cell_centre():
     err_cent = np.max(np.abs(g.get_coeffs() - ce))
     assert err_node < 1e-3 * err_cent * 10 and err_node < 2e-4, (err_node, err_cent)
     g.destroy()
+
+
+@pytest.mark.parametrize("seed", list(range(12)))
+def test_randomized_vnodes(seed):
+    """Random grids, k, (dim, vdim) pairs and node-velocity fields against the oracle."""
+    from paper_1603_07008_b200 import Grid
+    rng = np.random.default_rng(700 + seed)
+    D = int(rng.integers(2, 5))
+    k = int(rng.integers(1, 5))
+    dims = [int(rng.choice([1, 2, 3, 4, 6, 8, 12, 16, 33, 64])) for _ in range(D)]
+    while np.prod(dims) * k ** D > 400_000:
+        i = int(np.argmax(dims))
+        dims[i] = max(1, dims[i] // 2)
+    dim, vdim = [int(x) for x in rng.choice(D, 2, replace=False)]
+    precision = ["mixed", "fp64"][int(rng.integers(0, 2))]
+    K = k ** D
+    nd = 1 if (precision == "mixed" and K > 1) else K
+    c = sldg_inputs.random_coeffs(dims, k, seed)
+    src = oracle.round_layout(c, K, nd)
+    g = Grid(dims, k, precision=precision)
+    nv = dims[vdim]
+    # node shifts within one v-cell span at most ~2.5 cells (the kernel takes up to 6 offsets)
+    scale = min(float(rng.uniform(0.1, 1.2)) * dims[dim] / 4, 2.5 / (4.0 / nv))
+    nodal = vnodes.nodal_velocity_field(nv, -2.0, 2.0, k, scale)
+    g.set_coeffs(c)
+    g.advect_vnodes(dim, vdim, nodal)
+    ref = vnodes.advect_vnodes(src, dims, k, dim, vdim, nodal, n_double=nd)
+    _parity(g.get_coeffs(), ref, K, "fp64" if nd == K else "mixed", src, f"seed={seed} dims={dims} k={k}")
+    g.destroy()
