@@ -230,7 +230,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     sweep_dims = list(range(D)) if args.sweeps is None else [int(x) for x in args.sweeps.split(",")]
     cfg_json = {"workload": f"{args.config}: {desc}", "dims": dims, "k": k, "coeffs_per_cell": K,
-                "precision": args.precision, "ic": f"landau eps={args.eps}", "sweeps_per_step": len(sweep_dims),
+                "precision": args.precision,
+                "storage": "c0 fp64 + other coefficients fp32" if args.precision == "mixed" else "all fp64", "ic": f"landau eps={args.eps}", "sweeps_per_step": len(sweep_dims),
                 "parallelism": f"shard v{D // 2 if D > 2 else 1} (dim {D - 1}) x{world}" if world > 1 else "1 GPU",
                 "l2": "inputs larger than L2 (no flush needed)" if cells * bytes_per_cell(K, args.precision) > 4 * 126e6
                 else "inputs comparable to L2 (126 MB): L2 residency possible",
@@ -382,7 +383,7 @@ def main():
             "metric": "GDoF/s per advection sweep (split step of all dims)",
             "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": step_ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "f64 arithmetic; storage " + ("c0 fp64 + fp32" if args.precision == "mixed" else "fp64"),
+            "dtype": "f64",  # arithmetic type; storage is config.storage
             "data": "synthetic (Landau-type IC, Vlasov CFL fields)", "config": cfg_json,
             "hbm_gbs": alg_bytes_step / (step_ms * 1e-3) / 1e9 / world,
             "hbm_frac_of_peak": alg_bytes_step / (step_ms * 1e-3) / 1e9 / world / peak,
