@@ -231,10 +231,12 @@ def main():
     sweep_dims = list(range(D)) if args.sweeps is None else [int(x) for x in args.sweeps.split(",")]
     cfg_json = {"workload": f"{args.config}: {desc}", "dims": dims, "k": k, "coeffs_per_cell": K,
                 "precision": args.precision,
-                "storage": "c0 fp64 + other coefficients fp32" if args.precision == "mixed" else "all fp64", "ic": f"landau eps={args.eps}", "sweeps_per_step": len(sweep_dims),
+                "storage": "c0 fp64 + other coefficients fp32" if args.precision == "mixed" else "all fp64",
+                "ic": f"landau eps={args.eps}", "sweeps_per_step": len(sweep_dims),
                 "parallelism": f"shard v{D // 2 if D > 2 else 1} (dim {D - 1}) x{world}" if world > 1 else "1 GPU",
                 "l2": "inputs larger than L2 (no flush needed)" if cells * bytes_per_cell(K, args.precision) > 4 * 126e6
-                else "inputs comparable to L2 (126 MB): L2 residency possible",
+                else "source + destination arrays exceed L2 (126 MB) but one array is comparable: partial "
+                     "L2 residency between sweeps",
                 "dt": 0.1}
     if args.impl == "reference":
         return run_reference(args, dims, kinds, k, cfg_json)
