@@ -237,32 +237,35 @@ __device__ __forceinline__ void strided_group(const Layout& lay, const Arrays& s
             }
         }
     }
+    // per output slot j: all T targets at once, so each weight is loaded (from registers or,
+    // for large k, from L1) once and used for T targets (k >= 5 was load-bound one load per FMA)
 #pragma unroll
-    for (int p = 1; p <= T; ++p) {
-        if (p > nt) break;
-        const int64_t tm = g.t_m + (p - 1) * g.dt_m, tf = g.t_f + (p - 1) * g.dt_f;
+    for (int j = 0; j < KK; ++j) {
+        const int q = qbase + j * kd;
+        double o[T + 1];
 #pragma unroll
-        for (int j = 0; j < KK; ++j) {
-            const int q = qbase + j * kd;
-            double o;
-            if (cp) {
-                o = (j == 0) ? (double)v0[p] : (double)v[p][j];
-            } else {
-                o = 0.0;
+        for (int p = 1; p <= T; ++p) o[p] = cp ? ((j == 0) ? (double)v0[p] : (double)v[p][j]) : 0.0;
+        if (!cp) {
 #pragma unroll
-                for (int l = 0; l < KK; ++l) {
-                    const double wa = REGW ? wr[j * KK + l] : __ldg(&w[j * KK + l]);
-                    o = fma(wa, (l == 0) ? (double)v0[p - 1] : (double)v[p - 1][l], o);
-                }
+            for (int l = 0; l < KK; ++l) {
+                const double wa = REGW ? wr[j * KK + l] : __ldg(&w[j * KK + l]);
 #pragma unroll
-                for (int l = 0; l < KK; ++l) {
-                    const double wb = REGW ? wr[KK * KK + j * KK + l] : __ldg(&w[KK * KK + j * KK + l]);
-                    o = fma(wb, (l == 0) ? (double)v0[p] : (double)v[p][l], o);
-                }
+                for (int p = 1; p <= T; ++p) o[p] = fma(wa, (l == 0) ? (double)v0[p - 1] : (double)v[p - 1][l], o[p]);
             }
-            if (PREC == SLDG_FP64) __stcs(dst.s64 + tm + (int64_t)q * L, o);
-            else if (MASSG && j == 0) __stcs(dst.mass + tm, o);
-            else __stcs(dst.pl + tf + (int64_t)(q - 1) * L, __double2float_rn(o));
+#pragma unroll
+            for (int l = 0; l < KK; ++l) {
+                const double wb = REGW ? wr[KK * KK + j * KK + l] : __ldg(&w[KK * KK + j * KK + l]);
+#pragma unroll
+                for (int p = 1; p <= T; ++p) o[p] = fma(wb, (l == 0) ? (double)v0[p] : (double)v[p][l], o[p]);
+            }
+        }
+#pragma unroll
+        for (int p = 1; p <= T; ++p) {
+            if (p > nt) break;
+            const int64_t tm = g.t_m + (p - 1) * g.dt_m, tf = g.t_f + (p - 1) * g.dt_f;
+            if (PREC == SLDG_FP64) __stcs(dst.s64 + tm + (int64_t)q * L, o[p]);
+            else if (MASSG && j == 0) __stcs(dst.mass + tm, o[p]);
+            else __stcs(dst.pl + tf + (int64_t)(q - 1) * L, __double2float_rn(o[p]));
         }
     }
 }
