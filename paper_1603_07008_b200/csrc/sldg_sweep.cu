@@ -99,25 +99,33 @@ __device__ __forceinline__ void d0_batch(const Arrays& src, const Arrays& dst, i
             a[gb][j] = v;
         }
     if (!active) return;
+    // per output slot j: every group of the batch at once, so each weight load serves GB groups
 #pragma unroll
-    for (int gb = 0; gb < GB; ++gb) {
-        if (g0 + gb >= G) break;
+    for (int j = 0; j < KK; ++j) {
+        double o[GB];
 #pragma unroll
-        for (int j = 0; j < KK; ++j) {
-            const int q = (g0 + gb) * KK + j;
-            double o;
-            if (cp) {
-                o = b[gb][j];
-            } else {
-                o = 0.0;
+        for (int gb = 0; gb < GB; ++gb) o[gb] = cp ? b[gb][j] : 0.0;
+        if (!cp) {
 #pragma unroll
-                for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[j * KK + l]), a[gb][l], o);
+            for (int l = 0; l < KK; ++l) {
+                const double wa = __ldg(&w[j * KK + l]);
 #pragma unroll
-                for (int l = 0; l < KK; ++l) o = fma(__ldg(&w[KK * KK + j * KK + l]), b[gb][l], o);
+                for (int gb = 0; gb < GB; ++gb) o[gb] = fma(wa, a[gb][l], o[gb]);
             }
-            if (PREC == SLDG_FP64) __stcs(dst.s64 + mT + (int64_t)q * L, o);
-            else if (MASSG && gb == 0 && j == 0) __stcs(dst.mass + mT, o);
-            else __stcs(dst.pl + fT + (int64_t)(q - 1) * L, __double2float_rn(o));
+#pragma unroll
+            for (int l = 0; l < KK; ++l) {
+                const double wb = __ldg(&w[KK * KK + j * KK + l]);
+#pragma unroll
+                for (int gb = 0; gb < GB; ++gb) o[gb] = fma(wb, b[gb][l], o[gb]);
+            }
+        }
+#pragma unroll
+        for (int gb = 0; gb < GB; ++gb) {
+            if (g0 + gb >= G) break;
+            const int q = (g0 + gb) * KK + j;
+            if (PREC == SLDG_FP64) __stcs(dst.s64 + mT + (int64_t)q * L, o[gb]);
+            else if (MASSG && gb == 0 && j == 0) __stcs(dst.mass + mT, o[gb]);
+            else __stcs(dst.pl + fT + (int64_t)(q - 1) * L, __double2float_rn(o[gb]));
         }
     }
 }
@@ -382,7 +390,8 @@ static cudaError_t launch_sweep_k(const Layout& lay, const Sweep& sw, const Arra
 {
     const int threads = 256;
     if (sw.dim == 0) {
-        constexpr int GB = (KK <= 2) ? 6 : (KK <= 4 ? 12 / KK : 1);
+        // groups per thread (each weight load serves GB groups); measured on C3: k = 5 prefers 1
+        constexpr int GB = (KK <= 2) ? 6 : (KK <= 4 ? 12 / KK : (KK == 5 ? 1 : 2));
         int64_t total = (le - lb) * lay.L;
         if (total == 0) return cudaSuccess;
         int64_t blocks = (total + threads - 1) / threads;
