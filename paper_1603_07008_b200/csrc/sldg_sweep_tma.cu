@@ -752,7 +752,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                     mbar_wait(&empty[s], ph ^ 1);
                     const uint32_t es = (PREC == SLDG_FP64) ? 8u : 4u;
                     uint32_t bytes = (uint32_t)cell_stride * (BP * es + (massg ? 8u : 0u));
-                    if (g0 == 0) bytes += (uint32_t)(rv * recw * 8);
+                    if (g0 == 0) bytes += (uint32_t)((pl.rec1 ? 1 : rv) * recw * 8);
                     mbar_expect_tx(&full[s], bytes);
                     const int c1 = (int)(inner_base / box0);
                     if (massg) {
@@ -763,7 +763,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                         tma_5d(st, &tmaps.f[0], 0, c1, 0, plane0, (int)layerp, &full[s], pol);
                     }
                     if (g0 == 0) {
-                        for (int r = 0; r < rv; ++r) {  // the tile's line records
+                        for (int r = 0; r < (pl.rec1 ? 1 : rv); ++r) {  // the tile's line records
                             int64_t f = 0;
                             if (sw.fmask) {  // 32-bit index math: this thread feeds the whole CTA
                                 int64_t idx[kMaxDim];
@@ -787,7 +787,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
             } else {
                 mbar_wait(&full[s], ph);
                 if (g0 == 0 && has_cell) {  // this tile's line data for my line
-                    const double* rp = (const double*)(st + rec_off) + my_r * recw;
+                    const double* rp = (const double*)(st + rec_off) + (pl.rec1 ? 0 : my_r) * recw;
 #pragma unroll
                     for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = rp[i];
                     my_s = __double_as_longlong(rp[2 * KK * KK]);
@@ -946,6 +946,17 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
         if (GC * k > 256) return false;
         pl->R = (int)R;
         pl->GC = GC;
+        // the R lines of a tile share their field entry when every masked dim among 1..D-2
+        // changes only every (lines per step of that dim) % R == 0 lines: one record per tile
+        {
+            bool one = true;
+            int64_t stride = 1;  // lines per step of dim e
+            for (int e = 1; e < lay.D - 1; ++e) {
+                if ((sw.fmask >> e & 1u) && stride % R != 0) one = false;
+                stride *= lay.n[e];
+            }
+            pl->rec1 = one ? 1 : 0;
+        }
         // first box dim: the largest power of two <= 256 dividing cs and L (tiles start at
         // multiples of cs, so at multiples of W)
         int W = 256;
