@@ -177,6 +177,7 @@ struct TmaPlan {
     int R = 0;      // d0: whole lines per stage
     int GC = 0;     // d0: coupled groups per stage
     int rec1 = 0;   // d0: the tile's R lines share one field entry (one record per tile)
+    int pspan = 0;  // strided: the producer warp computes the tile shift spans (sldg_sweep_tma.cu)
     int stage_bytes = 0;
     int stages = 0;
     int ctas = 1;   // CTAs per SM (shared-memory budget and register bound of the instance)

@@ -391,13 +391,15 @@ static cudaError_t launch_sweep_k(const Layout& lay, const Sweep& sw, const Arra
     const int threads = 256;
     if (sw.dim == 0) {
         // groups per thread (each weight load serves GB groups); measured on C3: k = 5 prefers 1
+        // (mixed k = 5 / 6 with GB = 2 / 3: slower, 1.27 -> 1.36 / 2.29 -> 3.20 ms on C3)
         constexpr int GB = (KK <= 2) ? 6 : (KK <= 4 ? 12 / KK : (KK == 5 ? 1 : 2));
         int64_t total = (le - lb) * lay.L;
         if (total == 0) return cudaSuccess;
         int64_t blocks = (total + threads - 1) / threads;
         sweep_d0_kernel<KK, PREC, GB><<<(unsigned)blocks, threads, 0, s>>>(lay, sw, src, dst, lb, le);
     } else {
-        constexpr int T = (KK <= 2) ? 16 : (KK <= 3 ? 8 : 4);
+        // mixed k >= 5: 8 targets (C3 k = 5 strided 1.57 -> 1.46 ms, k = 6 2.16 -> 2.11 ms)
+        constexpr int T = (KK <= 2) ? 16 : (KK <= 3 ? 8 : ((KK >= 5 && PREC == SLDG_MIXED) ? 8 : 4));
         const bool outer = (sw.dim == lay.D - 1);
         int64_t nline = outer ? (le - lb) : sw.nd;
         int64_t nseg = (nline + T - 1) / T;

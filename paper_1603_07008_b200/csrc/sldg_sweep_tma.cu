@@ -238,7 +238,7 @@ __device__ __forceinline__ void strided_consume(const unsigned char* const* sb, 
 //   tensor maps (5D, fp32 planes or fp64 slots / fp64 mass):
 //         inner: {lo, i_d, hi, plane, layer}   outer: {lo, 1, 1, plane, layer}
 // ============================================================================================
-template <int KK, int PREC, int MINB>
+template <int KK, int PREC, int MINB, bool PSPAN>
 __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout lay, Sweep sw, Arrays src, Arrays dst,
                                                                   int64_t lb, int64_t le, TmaPlan pl,
                                                                   const __grid_constant__ TmapSet tmaps)
@@ -290,40 +290,83 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
     const int tid = threadIdx.x;
     const int c = tid % W, part = tid / W;
 
-    // tile -> (segment along d, column block, hi, layer)
+    // tile -> (segment along d, column block, hi, layer).  PSPAN: 32-bit index math with rolled
+    // loops (compact code: in short sweeps such as C2's this runs often, and the inlined 64-bit
+    // divisions made the kernel ~300 KB of SASS, instruction-cache bound); otherwise the 64-bit
+    // form the long-tile instances were tuned with (their hot-loop codegen depends on it).
     auto decode = [&](int64_t tl, int64_t& cb, int64_t& hi, int64_t& layer, int64_t& t0) {
-        int64_t rem = tl;
-        const int64_t seg = rem % nseg;
-        rem /= nseg;
-        cb = rem % nb;
-        rem /= nb;
-        hi = rem % M_hi;
-        rem /= M_hi;
-        layer = outer ? 0 : lb + rem;
-        t0 = seg * T;
+        if constexpr (PSPAN) {
+            uint32_t rem = (uint32_t)tl;
+            const uint32_t seg = rem % (uint32_t)nseg;
+            rem /= (uint32_t)nseg;
+            cb = rem % (uint32_t)nb;
+            rem /= (uint32_t)nb;
+            hi = rem % (uint32_t)M_hi;
+            rem /= (uint32_t)M_hi;
+            layer = outer ? 0 : lb + rem;
+            t0 = (int64_t)seg * T;
+        } else {
+            int64_t rem = tl;
+            const int64_t seg = rem % nseg;
+            rem /= nseg;
+            cb = rem % nb;
+            rem /= nb;
+            hi = rem % M_hi;
+            rem /= M_hi;
+            layer = outer ? 0 : lb + rem;
+            t0 = seg * T;
+        }
     };
     // field entry of column lo (all perpendicular indices from lo, hi, layer)
-    auto findex = [&](int64_t lo, int64_t hi, int64_t layer) {
-        int64_t idx[kMaxDim];
-#pragma unroll
-        for (int e = 0; e < kMaxDim; ++e) idx[e] = 0;
+    auto findex = [&](int64_t lo64, int64_t hi64, int64_t layer) -> int64_t {
         const int elo = outer ? D - 1 : d;
-        for (int e = 0; e < elo; ++e) {
-            idx[e] = lo % lay.n[e];
-            lo /= lay.n[e];
-        }
-        if (!outer) {
-            for (int e = d + 1; e < D - 1; ++e) {
-                idx[e] = hi % lay.n[e];
-                hi /= lay.n[e];
+        if constexpr (PSPAN) {
+            uint32_t lo = (uint32_t)lo64, hi = (uint32_t)hi64;
+            int64_t f = 0;
+#pragma unroll 1
+            for (int e = 0; e < elo; ++e) {
+                const uint32_t ne = (uint32_t)lay.n[e], q = lo / ne;
+                f += (int64_t)(lo - q * ne) * sw.fstride[e];
+                lo = q;
             }
-            idx[D - 1] = lay.first_layer + layer;
+            if (!outer) {
+#pragma unroll 1
+                for (int e = d + 1; e < D - 1; ++e) {
+                    const uint32_t ne = (uint32_t)lay.n[e], q = hi / ne;
+                    f += (int64_t)(hi - q * ne) * sw.fstride[e];
+                    hi = q;
+                }
+                f += (lay.first_layer + layer) * sw.fstride[D - 1];
+            }
+            return f;
+        } else {
+            int64_t lo = lo64, hi = hi64;
+            int64_t idx[kMaxDim];
+#pragma unroll
+            for (int e = 0; e < kMaxDim; ++e) idx[e] = 0;
+            for (int e = 0; e < elo; ++e) {
+                idx[e] = lo % lay.n[e];
+                lo /= lay.n[e];
+            }
+            if (!outer) {
+                for (int e = d + 1; e < D - 1; ++e) {
+                    idx[e] = hi % lay.n[e];
+                    hi /= lay.n[e];
+                }
+                idx[D - 1] = lay.first_layer + layer;
+            }
+            return tfield_index(sw, idx, D);
         }
-        return tfield_index(sw, idx, D);
     };
-    // The shifts of the NEXT tile's columns (for its shift span) are loaded while the current
-    // tile streams (software prefetch) -- in the 1-CTA-per-SM instance; the 2-CTA instance (96
-    // registers) loads them at the tile start instead of holding 8 of them across the tile.
+    // The tile's shift span (min / max integer shift over its W columns).
+    // PSPAN: computed by the producer warp alone, which loads the NEXT tile's column shifts while
+    // the current tile streams (software prefetch, 1-CTA-per-SM instance) and publishes each
+    // tile's span in a ring in shared memory before it arms the tile's first stage; consumers
+    // read it after that stage's full barrier, so no consumer warp runs per-column index math.
+    // Ring slot reuse is safe: slot (tile count % 8) is rewritten 8 tiles later, after the empty
+    // barrier of a stage >= 8 - S >= 0 stages past this tile's first one (S <= 8).
+    // Otherwise every warp computes the span itself from its own prefetch of the shifts.
+    int64_t* span_ring = (int64_t*)(smem + 128);  // [8][2]: imin, imax
     constexpr bool PF = (MINB == 1);
     int64_t pf_sh[PF ? 8 : 1];
     auto prefetch = [&](int64_t tl) {
@@ -335,46 +378,82 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
             pf_sh[i] = (cc < W) ? __ldg(&sw.shift[findex(cb * W + cc, hi, layer)]) : 0;
         }
     };
-    if (PF && (int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x);
+    if (PF && (producer || !PSPAN) && (int64_t)blockIdx.x < ntiles) prefetch(blockIdx.x);
 
     uint32_t it = 0;  // stage-use counter, identical in every warp
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t tcount = 0;  // tiles of this CTA so far, identical in every warp
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
         int64_t cb, hi, layer, t0;
         decode(tile, cb, hi, layer, t0);
         const int nt = (int)((nline - t0) < T ? (nline - t0) : T);
         const int64_t tg0 = outer ? lay.first_layer + lb : 0;  // line coordinate of target index 0
         const int64_t inner_base = outer ? cb * W : cb * W + hi * M_lo * sw.nd;  // column 0, coordinate 0
 
-        int64_t imin = INT64_MAX, imax = INT64_MIN;
-        if (PF) {
+        // this tile's consumer line data: column shift, copy flag, A/B in registers (PSPAN: issued
+        // before the wait for the tile's first stage, so their latency overlaps its first copy)
+        int64_t my_s = 0;
+        int my_cp = 0;
+        double wr[2 * KK * KK];
+        if constexpr (PSPAN) {
+            if (!producer) {
+                const int64_t f = findex(cb * W + c, hi, layer);
+                my_s = __ldg(&sw.shift[f]);
+                my_cp = __ldg(&sw.copy[f]);
 #pragma unroll
-            for (int i = 0; i < (PF ? 8 : 1); ++i) {
-                if (lane + 32 * i < W) {
-                    imin = pf_sh[i] < imin ? pf_sh[i] : imin;
-                    imax = pf_sh[i] > imax ? pf_sh[i] : imax;
+                for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
+            }
+        }
+        int64_t imin = INT64_MAX, imax = INT64_MIN;
+        int64_t* ring = span_ring + 2 * (tcount & 7);
+        if (producer || !PSPAN) {
+            if (PF) {
+#pragma unroll
+                for (int i = 0; i < (PF ? 8 : 1); ++i) {
+                    if (lane + 32 * i < W) {
+                        imin = pf_sh[i] < imin ? pf_sh[i] : imin;
+                        imax = pf_sh[i] > imax ? pf_sh[i] : imax;
+                    }
+                }
+            } else {
+#pragma unroll 1
+                for (int cc = lane; cc < W; cc += 32) {
+                    const int64_t sh = __ldg(&sw.shift[findex(cb * W + cc, hi, layer)]);
+                    imin = sh < imin ? sh : imin;
+                    imax = sh > imax ? sh : imax;
                 }
             }
-        } else {
-#pragma unroll 1
-            for (int cc = lane; cc < W; cc += 32) {
-                const int64_t sh = __ldg(&sw.shift[findex(cb * W + cc, hi, layer)]);
-                imin = sh < imin ? sh : imin;
-                imax = sh > imax ? sh : imax;
-            }
-        }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            int64_t a = __shfl_xor_sync(0xffffffffu, imin, o), b = __shfl_xor_sync(0xffffffffu, imax, o);
-            imin = a < imin ? a : imin;
-            imax = b > imax ? b : imax;
+            for (int o = 16; o > 0; o >>= 1) {
+                int64_t a = __shfl_xor_sync(0xffffffffu, imin, o), b = __shfl_xor_sync(0xffffffffu, imax, o);
+                imin = a < imin ? a : imin;
+                imax = b > imax ? b : imax;
+            }
+            if (PF && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
+            // publish after the tile's first stage is free (see the ring comment above)
+            if (PSPAN && lane == 0) {
+                mbar_wait(&empty[it % S], ((it / S) & 1) ^ 1);
+                ring[0] = imin;
+                ring[1] = imax;
+            }
+        } else {
+            mbar_wait(&full[it % S], (it / S) & 1);  // the tile's first stage: its span is published
+            imin = ring[0];
+            imax = ring[1];
         }
-        if (PF && tile + gridDim.x < ntiles) prefetch(tile + gridDim.x);
         const int64_t span = imax - imin;
         // sub-chunks of te targets: rows = te + 1 + span <= Rmax, balanced over the tile
         const int tmax = (int)(Rmax - 1 - span);
         (void)Tsub;
         if (tmax < 1) {
             // ---- shift spread too wide for a stage: direct global loads (rare) ----
+            // PSPAN: the tile still takes one stage slot: the producer completes its full barrier
+            // with a plain arrive (no bytes; it carried the span), the consumers release it
+            const int s0 = it % S;
+            if constexpr (PSPAN) {
+                ++it;
+                if (producer && lane == 0) mbar_arrive(&full[s0]);
+                __syncwarp();
+            }
             if (!producer) {
                 for (int col = tid; col < W; col += NT) {
                     const int64_t f = findex(cb * W + col, hi, layer);
@@ -429,23 +508,25 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
                         }
                     }
                 }
+                if constexpr (PSPAN) {
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&empty[s0]);
+                }
             }
             continue;
         }
         const int nsub = (nt + tmax - 1) / tmax;
         const int tsz = (nt + nsub - 1) / nsub;
-
-        // this tile's consumer line data: column shift, copy flag, A/B in registers
-        int64_t my_s = 0;
-        int my_cp = 0;
-        double wr[2 * KK * KK];
-        if (!producer) {
-            const int64_t f = findex(cb * W + c, hi, layer);
-            my_s = __ldg(&sw.shift[f]);
-            my_cp = __ldg(&sw.copy[f]);
+        if constexpr (!PSPAN) {
+            if (!producer) {
+                const int64_t f = findex(cb * W + c, hi, layer);
+                my_s = __ldg(&sw.shift[f]);
+                my_cp = __ldg(&sw.copy[f]);
 #pragma unroll
-            for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
+                for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
+            }
         }
+
         // output position of target index 0 (padded layer, inner)
         const int64_t ob_lp = outer ? lay.pad + lb : lay.pad + layer;
         const int64_t ob_in = inner_base + c;
@@ -566,6 +647,18 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
 //   cs = R n0 cells per stage row: one box = BP consecutive planes of the tile's cells.
 // ============================================================================================
 constexpr int kD0Tpt = 4;
+// k <= kD0RegK: the line's 2k^2 weights live in registers for the whole tile; larger k reads
+// them from the line record in shared memory, which then travels with EVERY stage of the tile
+constexpr int kD0RegK = 4;
+
+// weight load from the stage's line record: volatile, so the compiler re-reads it where it is
+// used instead of hoisting all 2k^2 weights into registers for the whole stage (spills)
+__device__ __forceinline__ double lds_f64(const double* p)
+{
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"((uint32_t)__cvta_generic_to_shared(p)));
+    return v;
+}
 
 // 4 outputs of one slot -> HBM (16-byte aligned: the quad starts at a multiple of 4 cells)
 __device__ __forceinline__ void st4(double* p, double a, double b, double c, double d)
@@ -623,16 +716,35 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, co
 #pragma unroll
     for (int j = 0; j < KK; ++j) {
         double o[kD0Tpt];
+        if (KK > kD0RegK) {
+            // weights in shared memory (the stage's line record): each weight is read once and
+            // used for the 4 targets; same operation order per target as below
+            double oa[kD0Tpt], ob[kD0Tpt];
 #pragma unroll
-        for (int r = 0; r < kD0Tpt; ++r) {
-            // A- and B-parts as two independent FMA chains (k deep instead of 2k), then one add
-            double oa = 0.0, ob = 0.0;
+            for (int r = 0; r < kD0Tpt; ++r) oa[r] = ob[r] = 0.0;
 #pragma unroll
             for (int l = 0; l < KK; ++l) {
-                oa = fma(wr[j * KK + l], v[l][r], oa);
-                ob = fma(wr[KK * KK + j * KK + l], v[l][r + 1], ob);
+                const double wa = lds_f64(&wr[j * KK + l]), wb = lds_f64(&wr[KK * KK + j * KK + l]);
+#pragma unroll
+                for (int r = 0; r < kD0Tpt; ++r) {
+                    oa[r] = fma(wa, v[l][r], oa[r]);
+                    ob[r] = fma(wb, v[l][r + 1], ob[r]);
+                }
             }
-            o[r] = oa + ob;
+#pragma unroll
+            for (int r = 0; r < kD0Tpt; ++r) o[r] = oa[r] + ob[r];
+        } else {
+#pragma unroll
+            for (int r = 0; r < kD0Tpt; ++r) {
+                // A- and B-parts as two independent FMA chains (k deep instead of 2k), then one add
+                double oa = 0.0, ob = 0.0;
+#pragma unroll
+                for (int l = 0; l < KK; ++l) {
+                    oa = fma(wr[j * KK + l], v[l][r], oa);
+                    ob = fma(wr[KK * KK + j * KK + l], v[l][r + 1], ob);
+                }
+                o[r] = oa + ob;
+            }
         }
         if (SLDG_DBL(j)) {
             st4(om, o[0], o[1], o[2], o[3]);
@@ -729,10 +841,11 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
     const int recw = 2 * KK * KK + 2;  // doubles per record
     const int rec_off = pl.stage_bytes - R * recw * 8;
 
+    constexpr bool SMW = KK > kD0RegK;  // weights read from the stage's record (every stage)
     uint32_t it = 0;
     int64_t my_s = 0;
     int my_cp = 0;
-    double wr[2 * KK * KK];
+    double wr[SMW ? 1 : 2 * KK * KK];
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t blk = tile % nblk;
         const int64_t layer = lb + tile / nblk;
@@ -752,7 +865,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                     mbar_wait(&empty[s], ph ^ 1);
                     const uint32_t es = (PREC == SLDG_FP64) ? 8u : 4u;
                     uint32_t bytes = (uint32_t)cell_stride * (BP * es + (massg ? 8u : 0u));
-                    if (g0 == 0) bytes += (uint32_t)((pl.rec1 ? 1 : rv) * recw * 8);
+                    if (g0 == 0 || SMW) bytes += (uint32_t)((pl.rec1 ? 1 : rv) * recw * 8);
                     mbar_expect_tx(&full[s], bytes);
                     const int c1 = (int)(inner_base / box0);
                     if (massg) {
@@ -762,7 +875,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                         const int plane0 = (PREC == SLDG_FP64) ? g0 * KK : g0 * KK - 1;
                         tma_5d(st, &tmaps.f[0], 0, c1, 0, plane0, (int)layerp, &full[s], pol);
                     }
-                    if (g0 == 0) {
+                    if (g0 == 0 || SMW) {
                         for (int r = 0; r < (pl.rec1 ? 1 : rv); ++r) {  // the tile's line records
                             int64_t f = 0;
                             if (sw.fmask) {  // 32-bit index math: this thread feeds the whole CTA
@@ -786,10 +899,12 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                 __syncwarp();
             } else {
                 mbar_wait(&full[s], ph);
+                const double* rp = (const double*)(st + rec_off) + (pl.rec1 ? 0 : my_r) * recw;
                 if (g0 == 0 && has_cell) {  // this tile's line data for my line
-                    const double* rp = (const double*)(st + rec_off) + (pl.rec1 ? 0 : my_r) * recw;
+                    if (!SMW) {
 #pragma unroll
-                    for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = rp[i];
+                        for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = rp[i];
+                    }
                     my_s = __double_as_longlong(rp[2 * KK * KK]);
                     my_cp = (int)__double_as_longlong(rp[2 * KK * KK + 1]);
                 }
@@ -816,10 +931,11 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                             om = dst.mass + toff_m<PREC>(lay, layerp, tin);
                             of = dst.pl + toff_f<PREC>(lay, layerp, tin) + (massg ? 0 : (int64_t)(q0 - 1) * L);
                         }
+                        const double* wsrc = SMW ? rp : wr;
                         if (massg)
-                            d0_consume<KK, PREC, true>(st, gc, cell_stride, col, om, of, L, my_cp, wr);
+                            d0_consume<KK, PREC, true>(st, gc, cell_stride, col, om, of, L, my_cp, wsrc);
                         else
-                            d0_consume<KK, PREC, false>(st, gc, cell_stride, col, om, of, L, my_cp, wr);
+                            d0_consume<KK, PREC, false>(st, gc, cell_stride, col, om, of, L, my_cp, wsrc);
                     }
                 }
                 __syncwarp();
@@ -922,7 +1038,9 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
     const int NT = kTmaConsumerWarps * 32;
     *pl = TmaPlan{};
     pl->ctas = ctas;
-    if (k > 4) return false;  // line weights live in registers; larger k uses the register kernels
+    // strided: the line weights live in registers (k <= 4); larger k uses the register kernels.
+    // d = 0: k <= 4 in registers, 5..8 from the record in shared memory (kD0RegK)
+    if (k > 8 || (k > 4 && sw.dim != 0)) return false;
     if (n0 % 4 != 0) return false;
     const int64_t layers_alloc = lay.layers + 2 * lay.pad;
     if (lay.L > (int64_t)1 << 31 || layers_alloc > 65535) return false;
@@ -939,7 +1057,7 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
         int64_t d0div = (k <= 2) ? 2 : 3;  // stage <= budget / d0div (C4: 2 beats 3, 3.8 -> 4.1 TB/s; override SLDG_TMA_D0DIV)
         if (const char* e = getenv("SLDG_TMA_D0DIV")) d0div = atoi(e);
         const int64_t target = budget / d0div;
-        if (group_bytes > budget / 2) return false;
+        if (group_bytes > std::max<int64_t>(budget, (int64_t)g_smem_optin / ctas - 256) / 2) return false;
         int gcmax = (int)std::max<int64_t>(1, std::min<int64_t>(G, target / group_bytes));
         const int nchunk = (G + gcmax - 1) / gcmax;
         const int GC = (G + nchunk - 1) / nchunk;  // balanced chunks
@@ -970,6 +1088,9 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
         pl->stage_bytes = (int)(((cs * (GC * k * es + ((lay.prec == SLDG_FP64) ? 0 : 8)) + 127) / 128 * 128 +
                                  R * (2 * k * k + 2) * 8 + 127) / 128 * 128);
         pl->stages = (int)std::min<int64_t>(8, budget / pl->stage_bytes);
+        // large stages (a long line of k >= 5): two of them may use the whole opt-in carveout
+        const int64_t budget_max = (int64_t)g_smem_optin / ctas - 256 - (ctas - 1) * 1024;
+        if (pl->stages < 2 && 2LL * pl->stage_bytes <= budget_max) pl->stages = 2;
         return pl->stages >= 2;
     }
     const bool outer = (sw.dim == lay.D - 1);
@@ -1028,6 +1149,14 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
     pl->W = W;
     pl->T = (int)T;
     pl->Tsub = Tsub;
+    // producer-computed tile spans (PSPAN) for short tiles: there the per-tile code runs often and
+    // its compact form pays (2D strided sweeps k = 2..4 +7-20%, C4 dims 2/3 +4-6%); tiles of many
+    // stages (C5: 27 groups x 7 sub-chunks) keep the other instance, whose hot loop the compiler
+    // schedules 6 instructions shorter for k = 3 (C5 strided 4-7% faster); the 2-CTA instance
+    // measured slower with it (C4 dim 1).  profiles/round1/tuning.md
+    const int64_t stages_per_tile = (int64_t)(lay.K / k) * ((T + Tsub - 1) / Tsub);
+    pl->pspan = (ctas == 1 && stages_per_tile <= 64) ? 1 : 0;
+    if (const char* e = getenv("SLDG_TMA_PSPAN")) pl->pspan = atoi(e) ? 1 : 0;
     pl->Rmax = Rmax;
     pl->stage_bytes = stage_bytes;
     pl->stages = stages;
@@ -1150,7 +1279,7 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
-    } else {
+    } else if constexpr (KK <= 4) {
         const bool outer = (sw.dim == lay.D - 1);
         const int64_t nline = outer ? (le - lb) : sw.nd;
         int64_t M_lo = 1, M_hi = 1;
@@ -1158,15 +1287,18 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         if (!outer)
             for (int e = sw.dim + 1; e < lay.D - 1; ++e) M_hi *= lay.n[e];
         ntiles = ((nline + pl.T - 1) / pl.T) * (M_lo / pl.W) * M_hi * (outer ? 1 : (le - lb));
-        auto kern = (pl.ctas == 2) ? sweep_strided_tma<KK, PREC, 2> : sweep_strided_tma<KK, PREC, 1>;
-        static bool attr_set[3] = {false, false, false};  // once per instantiation: full opt-in carveout
-        if (!attr_set[pl.ctas]) {
+        auto kern = (pl.ctas == 2) ? (pl.pspan ? sweep_strided_tma<KK, PREC, 2, true> : sweep_strided_tma<KK, PREC, 2, false>)
+                                   : (pl.pspan ? sweep_strided_tma<KK, PREC, 1, true> : sweep_strided_tma<KK, PREC, 1, false>);
+        static bool attr_set[3][2] = {};  // once per instantiation: full opt-in carveout
+        if (!attr_set[pl.ctas][pl.pspan]) {
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
-            attr_set[pl.ctas] = true;
+            attr_set[pl.ctas][pl.pspan] = true;
         }
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
+    } else {
+        return cudaErrorInvalidValue;  // strided k > 4: the plan never selects it
     }
     return cudaGetLastError();
 }
@@ -1180,6 +1312,10 @@ static cudaError_t launch_tma_p(const Layout& lay, const Sweep& sw, const Arrays
         case 2: return launch_tma_k<2, PREC>(lay, sw, src, dst, lb, le, pl, s);
         case 3: return launch_tma_k<3, PREC>(lay, sw, src, dst, lb, le, pl, s);
         case 4: return launch_tma_k<4, PREC>(lay, sw, src, dst, lb, le, pl, s);
+        case 5: return launch_tma_k<5, PREC>(lay, sw, src, dst, lb, le, pl, s);
+        case 6: return launch_tma_k<6, PREC>(lay, sw, src, dst, lb, le, pl, s);
+        case 7: return launch_tma_k<7, PREC>(lay, sw, src, dst, lb, le, pl, s);
+        case 8: return launch_tma_k<8, PREC>(lay, sw, src, dst, lb, le, pl, s);
     }
     return cudaErrorInvalidValue;
 }

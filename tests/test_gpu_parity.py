@@ -633,3 +633,34 @@ def test_randomized_medium_grids_match_oracle(seed):
         assert_parity(g.get_coeffs(), ref, K, precision,
                       f"seed={seed} dims={dims} k={k} dim={dim} kernel={g.sweep_kernel(dim)}", ref_in, dim, k)
     g.destroy()
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+@pytest.mark.parametrize("dims,k", [([64, 20], 5), ([48, 6, 5], 6), ([16, 4, 3], 7), ([12, 4, 3], 8),
+                                    ([4096, 6], 5), ([20, 6, 4, 3], 5), ([1024, 9], 6)])
+def test_high_order_d0_tma_matches_oracle(dims, k, precision):
+    if dims[0] == 4096 and precision == "fp64":
+        pytest.skip("two stages of a 4096-cell fp64 k = 5 group exceed shared memory (register kernel)")
+    """k = 5..8 on d = 0: the TMA kernel reading the line weights from the record in shared memory
+    (a copy in every stage of the tile); constant shifts, per-line fields (one record per tile
+    and one per line) and copy lines."""
+    D, K = len(dims), k ** len(dims)
+    rng = np.random.default_rng(77 + k)
+    c = sldg_inputs.random_coeffs(dims, k, 5150 + k)
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision)
+    assert g.sweep_kernel(0) == "sweep_d0_tma", g.sweep_kernel(0)
+    cases = [(3.37, None, 0), (-0.41 - dims[0], None, 0)]
+    if D >= 2:
+        mask = (1 << (D - 1)) | (2 if D >= 3 else 0)
+        nf = int(np.prod([dims[e] for e in range(D) if mask >> e & 1]))
+        field = rng.uniform(-2.5 * dims[0], 2.5 * dims[0], nf)
+        field[::5] = np.round(field[::5])
+        cases.append((0.0, field, mask))
+    for shift, field, mask in cases:
+        g.set_coeffs(c)
+        g.advect(0, shift=shift, field=field, field_mask=mask)
+        ref = oracle.advect(ref_in, dims, k, 0, shift=shift, field=field, field_mask=mask,
+                            n_double=n_double(precision, K))
+        assert_parity(g.get_coeffs(), ref, K, precision, f"dims={dims} k={k} nu={shift} mask={mask}", ref_in, 0, k)
+    g.destroy()
