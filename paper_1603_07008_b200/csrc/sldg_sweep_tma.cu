@@ -230,6 +230,88 @@ __device__ __forceinline__ void strided_consume(const unsigned char* const* sb, 
 #undef SLDG_DBL
 }
 
+// Split variant for k >= 5 (the 2k^2 weights of a whole line do not fit in registers next to the
+// walk): SPL = 2 threads share a column, thread J0 / JN owns output slots [J0, J0 + JN) and their
+// JN rows of A and B (wr[jj * KK + l] = A[J0 + jj][l], wr[JN * KK + jj * KK + l] = B[J0 + jj][l]);
+// both read all k inputs of every row.  Same operation order per output as strided_consume.
+template <int KK, int PREC, bool MASSG, int JN, int J0>
+__device__ __forceinline__ void strided_consume_split(const unsigned char* const* sb, int sstride, int rB0, int cnt,
+                                                      char* const* op, int64_t ostep_m, int64_t ostep_f, int cp,
+                                                      const double* wr)
+{
+#define SLDG_DBL(j) ((PREC == SLDG_FP64) || (MASSG && (j) == 0))
+    const unsigned char* rp[KK];
+    char* wp[JN];
+    int64_t wstep[JN];
+#pragma unroll
+    for (int j = 0; j < KK; ++j) rp[j] = sb[j] + (int64_t)(rB0 - 1) * sstride * (SLDG_DBL(j) ? 8 : 4);
+#pragma unroll
+    for (int jj = 0; jj < JN; ++jj) {
+        const int j = J0 + jj;
+        wp[jj] = (j < KK) ? op[j < KK ? j : 0] : nullptr;
+        wstep[jj] = SLDG_DBL(j) ? ostep_m * 8 : ostep_f * 4;
+    }
+    const int rstep = sstride;
+    if (cp) {
+        for (int u = 0; u < cnt; ++u) {
+#pragma unroll
+            for (int j = 0; j < KK; ++j) rp[j] += rstep * (SLDG_DBL(j) ? 8 : 4);
+#pragma unroll
+            for (int jj = 0; jj < JN; ++jj) {
+                const int j = J0 + jj;
+                if (j >= KK) break;
+                if (SLDG_DBL(j)) __stcs((double*)wp[jj], *(const double*)rp[j]);
+                else __stcs((float*)wp[jj], *(const float*)rp[j]);
+                wp[jj] += wstep[jj];
+            }
+        }
+        return;
+    }
+    double sA[JN], vb[KK];
+    {
+        double va[KK];
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            va[j] = SLDG_DBL(j) ? *(const double*)rp[j] : (double)*(const float*)rp[j];
+            rp[j] += rstep * (SLDG_DBL(j) ? 8 : 4);
+        }
+#pragma unroll
+        for (int jj = 0; jj < JN; ++jj) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < KK; ++l) s = fma(wr[jj * KK + l], va[l], s);
+            sA[jj] = s;
+        }
+    }
+#pragma unroll 1
+    for (int u = 0; u < cnt; ++u) {
+#pragma unroll
+        for (int j = 0; j < KK; ++j) {
+            vb[j] = SLDG_DBL(j) ? *(const double*)rp[j] : (double)*(const float*)rp[j];
+            rp[j] += rstep * (SLDG_DBL(j) ? 8 : 4);
+        }
+#pragma unroll
+        for (int jj = 0; jj < JN; ++jj) {
+            const int j = J0 + jj;
+            if (j >= KK) break;
+            double o = sA[jj];
+#pragma unroll
+            for (int l = 0; l < KK; ++l) o = fma(wr[JN * KK + jj * KK + l], vb[l], o);
+            if (SLDG_DBL(j)) __stcs((double*)wp[jj], o);
+            else __stcs((float*)wp[jj], __double2float_rn(o));
+            wp[jj] += wstep[jj];
+        }
+#pragma unroll
+        for (int jj = 0; jj < JN; ++jj) {
+            double s = 0.0;
+#pragma unroll
+            for (int l = 0; l < KK; ++l) s = fma(wr[jj * KK + l], vb[l], s);
+            sA[jj] = s;
+        }
+    }
+#undef SLDG_DBL
+}
+
 // ============================================================================================
 // strided sweep (d >= 1)
 //   lo  = linear index over the dims below d (outer sweep: all dims below D-1), contiguous in
@@ -286,9 +368,13 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
     const int64_t tstep_f = outer ? (toff_f<PREC>(lay, 1, 0) - toff_f<PREC>(lay, 0, 0)) : M_lo;
 
     const int NT = NC * 32;
-    const int P = NT / W;
+    // k >= 5: SPL = 2 threads per column, each with half of the output slots (W <= NT / 2)
+    constexpr int SPL = (KK > 4) ? 2 : 1;
+    constexpr int JN = (KK + SPL - 1) / SPL;
+    const int P = NT / (W * SPL);
     const int tid = threadIdx.x;
-    const int c = tid % W, part = tid / W;
+    const int c = tid % W, part = tid / (W * SPL);
+    const int jh = (SPL == 1) ? 0 : (tid / W) % SPL;
 
     // tile -> (segment along d, column block, hi, layer).  PSPAN: 32-bit index math with rolled
     // loops (compact code: in short sweeps such as C2's this runs often, and the inlined 64-bit
@@ -393,14 +479,26 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
         // before the wait for the tile's first stage, so their latency overlaps its first copy)
         int64_t my_s = 0;
         int my_cp = 0;
-        double wr[2 * KK * KK];
+        double wr[2 * JN * KK];
         if constexpr (PSPAN) {
             if (!producer) {
                 const int64_t f = findex(cb * W + c, hi, layer);
                 my_s = __ldg(&sw.shift[f]);
                 my_cp = __ldg(&sw.copy[f]);
+                if constexpr (SPL == 1) {
 #pragma unroll
-                for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
+                    for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < JN; ++jj) {
+                        const int j = jh * JN + jj < KK ? jh * JN + jj : KK - 1;
+#pragma unroll
+                        for (int l = 0; l < KK; ++l) {
+                            wr[jj * KK + l] = __ldg(&sw.ab[f * (2 * KK * KK) + j * KK + l]);
+                            wr[JN * KK + jj * KK + l] = __ldg(&sw.ab[f * (2 * KK * KK) + KK * KK + j * KK + l]);
+                        }
+                    }
+                }
             }
         }
         int64_t imin = INT64_MAX, imax = INT64_MIN;
@@ -522,8 +620,20 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
                 const int64_t f = findex(cb * W + c, hi, layer);
                 my_s = __ldg(&sw.shift[f]);
                 my_cp = __ldg(&sw.copy[f]);
+                if constexpr (SPL == 1) {
 #pragma unroll
-                for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
+                    for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = __ldg(&sw.ab[f * (2 * KK * KK) + i]);
+                } else {
+#pragma unroll
+                    for (int jj = 0; jj < JN; ++jj) {
+                        const int j = jh * JN + jj < KK ? jh * JN + jj : KK - 1;
+#pragma unroll
+                        for (int l = 0; l < KK; ++l) {
+                            wr[jj * KK + l] = __ldg(&sw.ab[f * (2 * KK * KK) + j * KK + l]);
+                            wr[JN * KK + jj * KK + l] = __ldg(&sw.ab[f * (2 * KK * KK) + KK * KK + j * KK + l]);
+                        }
+                    }
+                }
             }
         }
 
@@ -623,10 +733,22 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
                             op[j] = slot_ptr_w<PREC>(dst, lay, q, ob_lp, ob_in) +
                                     (int64_t)tl0 * (es == 8 ? tstep_m * 8 : tstep_f * 4);
                         }
-                        if (massg)
-                            strided_consume<KK, PREC, true>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
-                        else
-                            strided_consume<KK, PREC, false>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
+                        if constexpr (SPL == 1) {
+                            if (massg)
+                                strided_consume<KK, PREC, true>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
+                            else
+                                strided_consume<KK, PREC, false>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
+                        } else if (jh == 0) {
+                            if (massg)
+                                strided_consume_split<KK, PREC, true, JN, 0>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
+                            else
+                                strided_consume_split<KK, PREC, false, JN, 0>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
+                        } else {
+                            if (massg)
+                                strided_consume_split<KK, PREC, true, JN, JN>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
+                            else
+                                strided_consume_split<KK, PREC, false, JN, JN>(sb, W, rB0, hi_t - lo_t, op, tstep_m, tstep_f, my_cp, wr);
+                        }
                     }
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&empty[s]);
@@ -864,13 +986,14 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
                 if (lane == 0) {
                     mbar_wait(&empty[s], ph ^ 1);
                     const uint32_t es = (PREC == SLDG_FP64) ? 8u : 4u;
-                    uint32_t bytes = (uint32_t)cell_stride * (BP * es + (massg ? 8u : 0u));
+                    // the mass group: fp64 mass + the group's BP - 1 fp32 planes (tensor map 1)
+                    uint32_t bytes = (uint32_t)cell_stride * (massg ? (BP - 1) * 4u + 8u : BP * es);
                     if (g0 == 0 || SMW) bytes += (uint32_t)((pl.rec1 ? 1 : rv) * recw * 8);
                     mbar_expect_tx(&full[s], bytes);
                     const int c1 = (int)(inner_base / box0);
                     if (massg) {
                         tma_5d(st, &tmaps.m[0], 0, c1, 0, 0, (int)layerp, &full[s], pol);
-                        tma_5d(st + cell_stride * 8, &tmaps.f[0], 0, c1, 0, 0, (int)layerp, &full[s], pol);
+                        tma_5d(st + cell_stride * 8, &tmaps.f[1], 0, c1, 0, 0, (int)layerp, &full[s], pol);
                     } else {
                         const int plane0 = (PREC == SLDG_FP64) ? g0 * KK : g0 * KK - 1;
                         tma_5d(st, &tmaps.f[0], 0, c1, 0, plane0, (int)layerp, &full[s], pol);
@@ -1038,9 +1161,13 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
     const int NT = kTmaConsumerWarps * 32;
     *pl = TmaPlan{};
     pl->ctas = ctas;
-    // strided: the line weights live in registers (k <= 4); larger k uses the register kernels.
+    // strided: the line weights live in registers (k <= 4 one thread per column, k = 5, 6 two
+    // threads per column with half the output slots each); k >= 7 uses the register kernels.
     // d = 0: k <= 4 in registers, 5..8 from the record in shared memory (kD0RegK)
-    if (k > 8 || (k > 4 && sw.dim != 0)) return false;
+    if (k > 8 || (k > 6 && sw.dim != 0)) return false;
+    // fp64 k = 5, 6 strided: the register kernel is faster (C3: 1.12 / 1.59 ms vs 1.25 / 1.82 ms
+    // split TMA, whose two threads per column both read every fp64 input row)
+    if (k > 4 && sw.dim != 0 && lay.prec == SLDG_FP64) return false;
     if (n0 % 4 != 0) return false;
     const int64_t layers_alloc = lay.layers + 2 * lay.pad;
     if (lay.L > (int64_t)1 << 31 || layers_alloc > 65535) return false;
@@ -1082,10 +1209,12 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
         if (cs % W != 0 || lay.L % W != 0 || cs / W > 256) return false;
         pl->W = W;
         const int es = (lay.prec == SLDG_FP64) ? 8 : 4;
-        // stage: [mass (mixed mass group)] + GC*k planes (the mass group's box holds one spare plane)
-        // + the tile's R packed line records at the end (16-byte aligned: 16(k^2+1) bytes each)
-        // (stage starts stay 128-byte aligned for the tensor copies; records end the stage)
-        pl->stage_bytes = (int)(((cs * (GC * k * es + ((lay.prec == SLDG_FP64) ? 0 : 8)) + 127) / 128 * 128 +
+        // stage: GC*k planes, or for the mixed mass group the fp64 mass + GC*k - 1 fp32 planes
+        // (max: GC*k*4 + 4 bytes per cell), + the tile's R packed line records at the end
+        // (16-byte aligned: 16(k^2+1) bytes each; stage starts stay 128-byte aligned for the
+        // tensor copies; records end the stage)
+        if (lay.prec != SLDG_FP64 && GC * k < 2) return false;
+        pl->stage_bytes = (int)(((cs * (GC * k * es + ((lay.prec == SLDG_FP64) ? 0 : 4)) + 127) / 128 * 128 +
                                  R * (2 * k * k + 2) * 8 + 127) / 128 * 128);
         pl->stages = (int)std::min<int64_t>(8, budget / pl->stage_bytes);
         // large stages (a long line of k >= 5): two of them may use the whole opt-in carveout
@@ -1116,6 +1245,7 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
     const int64_t nline_p = outer ? lay.layers : sw.nd;
     for (int w : {256, 128, 64, 32}) {
         if (M_lo % w != 0 || w > Wmax) continue;
+        if (k > 4 && w > NT / 2) continue;  // two threads per column (strided_consume_split)
         int ts = (int)std::min<int64_t>(Tsub0, budget / sdiv / ((int64_t)w * bpc_max) - 4);
         if (ts < 4) continue;
         W = w;
@@ -1179,6 +1309,9 @@ static bool build_tmaps(const Layout& lay, const Sweep& sw, const Arrays& src, c
         const int bx[5] = {(int)b0, (int)(cs / b0), 1, pl.GC * lay.k, 1};
         if (!make_tmap(&ts->f[0], f64, fbase, dm, sm, bx)) return false;
         if (!f64) {
+            // the mass group's planes: slots 1 .. GC k - 1 (no spare plane in its stage)
+            const int bx1[5] = {(int)b0, (int)(cs / b0), 1, pl.GC * lay.k - 1, 1};
+            if (!make_tmap(&ts->f[1], f64, fbase, dm, sm, bx1)) return false;
             const int64_t dmm[5] = {b0, L / b0, 1, 1, layers_alloc};
             const int64_t smm[5] = {1, b0, L, L, L};
             const int bxm[5] = {(int)b0, (int)(cs / b0), 1, 1, 1};
@@ -1279,7 +1412,7 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
-    } else if constexpr (KK <= 4) {
+    } else if constexpr (KK <= 6) {
         const bool outer = (sw.dim == lay.D - 1);
         const int64_t nline = outer ? (le - lb) : sw.nd;
         int64_t M_lo = 1, M_hi = 1;

@@ -664,3 +664,31 @@ def test_high_order_d0_tma_matches_oracle(dims, k, precision):
                             n_double=n_double(precision, K))
         assert_parity(g.get_coeffs(), ref, K, precision, f"dims={dims} k={k} nu={shift} mask={mask}", ref_in, 0, k)
     g.destroy()
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+@pytest.mark.parametrize("dims,k", [([64, 20], 5), ([32, 12, 6], 6), ([128, 9], 5), ([64, 8, 4, 3], 5),
+                                    ([256, 40], 6)])
+def test_high_order_strided_tma_matches_oracle(dims, k, precision):
+    """k = 5, 6 on strided sweeps: the TMA kernel with two threads per column, each owning half of
+    the output slots and their rows of A, B; constant shifts of both signs, per-lane fields over
+    dim 0 (spans of several cells) and copy lines."""
+    D, K = len(dims), k ** len(dims)
+    rng = np.random.default_rng(91 + k + D)
+    c = sldg_inputs.random_coeffs(dims, k, 6150 + k)
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision)
+    for dim in range(1, D):
+        want = "sweep_strided_tma" if precision == "mixed" else "sweep_strided_kernel"  # fp64: register kernel
+        assert g.sweep_kernel(dim) == want, (dim, g.sweep_kernel(dim))
+        f0 = rng.uniform(-3.2, 3.2, dims[0])
+        f0[::6] = np.round(f0[::6])
+        cases = [(2.37, None, 0), (-0.63 - dims[dim], None, 0), (0.0, f0, 1)]
+        for shift, field, mask in cases:
+            g.set_coeffs(c)
+            g.advect(dim, shift=shift, field=field, field_mask=mask)
+            ref = oracle.advect(ref_in, dims, k, dim, shift=shift, field=field, field_mask=mask,
+                                n_double=n_double(precision, K))
+            assert_parity(g.get_coeffs(), ref, K, precision, f"dims={dims} k={k} dim={dim} nu={shift} mask={mask}",
+                          ref_in, dim, k)
+    g.destroy()
