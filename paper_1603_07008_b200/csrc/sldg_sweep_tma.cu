@@ -835,12 +835,12 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, co
             sp += cs * 4;
         }
     }
-#pragma unroll
-    for (int j = 0; j < KK; ++j) {
-        double o[kD0Tpt];
-        if (KK > kD0RegK) {
-            // weights in shared memory (the stage's line record): each weight is read once and
-            // used for the 4 targets; same operation order per target as below
+    if constexpr (KK > kD0RegK) {
+        // weights in shared memory (the stage's line record): each weight is read once and used
+        // for the 4 targets; same operation order per target as below.  One output slot per
+        // iteration (not unrolled: unrolled, the k = 6 body spilled ~230 registers)
+#pragma unroll 1
+        for (int j = 0; j < KK; ++j) {
             double oa[kD0Tpt], ob[kD0Tpt];
 #pragma unroll
             for (int r = 0; r < kD0Tpt; ++r) oa[r] = ob[r] = 0.0;
@@ -853,9 +853,19 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, co
                     ob[r] = fma(wb, v[l][r + 1], ob[r]);
                 }
             }
+            if (SLDG_DBL(j)) {
+                st4(om, oa[0] + ob[0], oa[1] + ob[1], oa[2] + ob[2], oa[3] + ob[3]);
+                om += L;
+            } else {
+                st4(of, __double2float_rn(oa[0] + ob[0]), __double2float_rn(oa[1] + ob[1]),
+                    __double2float_rn(oa[2] + ob[2]), __double2float_rn(oa[3] + ob[3]));
+                of += L;
+            }
+        }
+    } else {
 #pragma unroll
-            for (int r = 0; r < kD0Tpt; ++r) o[r] = oa[r] + ob[r];
-        } else {
+        for (int j = 0; j < KK; ++j) {
+            double o[kD0Tpt];
 #pragma unroll
             for (int r = 0; r < kD0Tpt; ++r) {
                 // A- and B-parts as two independent FMA chains (k deep instead of 2k), then one add
@@ -867,14 +877,14 @@ __device__ __forceinline__ void d0_group(const unsigned char*& sp, int cs_rt, co
                 }
                 o[r] = oa + ob;
             }
-        }
-        if (SLDG_DBL(j)) {
-            st4(om, o[0], o[1], o[2], o[3]);
-            om += L;
-        } else {
-            st4(of, __double2float_rn(o[0]), __double2float_rn(o[1]), __double2float_rn(o[2]),
-                __double2float_rn(o[3]));
-            of += L;
+            if (SLDG_DBL(j)) {
+                st4(om, o[0], o[1], o[2], o[3]);
+                om += L;
+            } else {
+                st4(of, __double2float_rn(o[0]), __double2float_rn(o[1]), __double2float_rn(o[2]),
+                    __double2float_rn(o[3]));
+                of += L;
+            }
         }
     }
 #undef SLDG_DBL
