@@ -283,7 +283,7 @@ __device__ __forceinline__ void strided_consume_split(const unsigned char* const
             sA[jj] = s;
         }
     }
-#pragma unroll 1
+#pragma unroll 2
     for (int u = 0; u < cnt; ++u) {
 #pragma unroll
         for (int j = 0; j < KK; ++j) {
