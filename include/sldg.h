@@ -33,7 +33,8 @@
  * sldg_last_error() returns a thread-local message for the last failure on this thread.
  * EINVAL failures leave the grid unchanged.  Ownership: the handle owns all device memory
  * it allocates (and the NCCL communicator if it created one); the caller owns all host
- * buffers, which are never retained after a call returns.
+ * buffers, which are never retained after a call returns (a host shift field is copied into
+ * the handle's pinned staging ring before sldg_advect returns, pinned caller memory included).
  * Threading: a handle is not thread-safe; distinct handles are independent.  When the grid
  * is distributed (world > 1) every call except sldg_last_error / sldg_memory_bytes /
  * sldg_shard_info is collective and must be made in the same order on all ranks.

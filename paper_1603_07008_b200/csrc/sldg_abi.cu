@@ -119,6 +119,39 @@ sldg_status ensure_field(sldg_grid g, int64_t n)
     return SLDG_OK;
 }
 
+// Host shift field -> g->d_field, asynchronously, without retaining the caller's pointer: the
+// entries are copied into a pinned staging slot (a ring of kFieldStages; a slot is reused once
+// the event after its upload has completed) and uploaded from there on the grid's stream.
+static sldg_status upload_host_field(sldg_grid g, const double* field, int64_t n)
+{
+    sldg_status st = ensure_field(g, n);
+    if (st != SLDG_OK) return st;
+    constexpr int NS = sldg_grid_s::kFieldStages;
+    if (g->fstage_cap < n) {
+        for (int s = 0; s < NS; ++s) {
+            if (g->fstage_busy[s]) CU(cudaEventSynchronize(g->fstage_ev[s]));
+            g->fstage_busy[s] = false;
+            if (g->h_fstage[s]) cudaFreeHost(g->h_fstage[s]);
+            g->h_fstage[s] = nullptr;
+        }
+        g->fstage_cap = 0;
+        const int64_t cap = std::max<int64_t>(n, 64);
+        for (int s = 0; s < NS; ++s) {
+            CU(cudaHostAlloc((void**)&g->h_fstage[s], cap * sizeof(double), cudaHostAllocDefault));
+            if (!g->fstage_ev[s]) CU(cudaEventCreateWithFlags(&g->fstage_ev[s], cudaEventDisableTiming));
+        }
+        g->fstage_cap = cap;
+    }
+    const int s = g->fstage_next;
+    g->fstage_next = (s + 1) % NS;
+    if (g->fstage_busy[s]) CU(cudaEventSynchronize(g->fstage_ev[s]));
+    memcpy(g->h_fstage[s], field, (size_t)n * sizeof(double));
+    CU(cudaMemcpyAsync(g->d_field, g->h_fstage[s], (size_t)n * sizeof(double), cudaMemcpyHostToDevice, g->stream));
+    CU(cudaEventRecord(g->fstage_ev[s], g->stream));
+    g->fstage_busy[s] = true;
+    return SLDG_OK;
+}
+
 sldg_status ensure_stage(sldg_grid g)
 {
     if (g->d_stage) return SLDG_OK;
@@ -506,9 +539,8 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
         if (field_on_device) {
             dfield = field;
         } else {
-            st = ensure_field(g, n_entries);
+            st = upload_host_field(g, field, n_entries);
             if (st != SLDG_OK) return st;
-            CU(cudaMemcpyAsync(g->d_field, field, n_entries * sizeof(double), cudaMemcpyHostToDevice, g->stream));
             dfield = g->d_field;
         }
     }
@@ -868,6 +900,10 @@ sldg_status sldg_destroy(sldg_grid g)
     cudaFree(g->w.ab);
     cudaFree(g->w.rec);
     cudaFree(g->d_field);
+    for (int s = 0; s < sldg_grid_s::kFieldStages; ++s) {
+        if (g->h_fstage[s]) cudaFreeHost(g->h_fstage[s]);
+        if (g->fstage_ev[s]) cudaEventDestroy(g->fstage_ev[s]);
+    }
     cudaFree(g->d_partials);
     cudaFree(g->d_scalar);
     cudaFree(g->d_err);

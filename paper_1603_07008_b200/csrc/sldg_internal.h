@@ -101,6 +101,14 @@ struct Grid {
     int64_t w_n = 0;
     double* d_field = nullptr;
     int64_t field_cap = 0;
+    // pinned staging ring for host shift fields: the caller's buffer is copied on the host before
+    // sldg_advect returns (never read later by a DMA), then uploaded asynchronously
+    static constexpr int kFieldStages = 4;
+    double* h_fstage[kFieldStages] = {};
+    cudaEvent_t fstage_ev[kFieldStages] = {};
+    bool fstage_busy[kFieldStages] = {};
+    int64_t fstage_cap = 0;
+    int fstage_next = 0;
     double* d_partials = nullptr;  // mass partial sums
     double* d_scalar = nullptr;    // misc device scalars
     int* d_err = nullptr;          // sticky device error flag

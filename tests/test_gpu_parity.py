@@ -692,3 +692,33 @@ def test_high_order_strided_tma_matches_oracle(dims, k, precision):
             assert_parity(g.get_coeffs(), ref, K, precision, f"dims={dims} k={k} dim={dim} nu={shift} mask={mask}",
                           ref_in, dim, k)
     g.destroy()
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+def test_host_field_not_retained(precision):
+    """sldg_advect copies a host shift field before it returns (the library never
+    retains host pointers): overwriting a PINNED host buffer right after the call -- before the
+    GPU has run the sweep -- must not change the result; several calls back to back cycle the
+    staging ring."""
+    import torch
+    dims, k = [256, 96], 3
+    K = k ** 2
+    c = sldg_inputs.random_coeffs(dims, k, 4242)
+    ref_in = oracle_input(c, K, precision)
+    rng = np.random.default_rng(17)
+    fields = [rng.uniform(-5.0, 5.0, dims[0]) for _ in range(7)]
+    g = _Grid(dims, k, precision=precision)
+    g.set_coeffs(c)
+    buf = torch.empty(dims[0], dtype=torch.float64, pin_memory=True)
+    hv = buf.numpy()
+    for f in fields:  # v-sweeps with per-lane fields, host buffer clobbered after every call
+        hv[:] = f
+        g.advect(1, field=hv, field_mask=1)
+        hv[:] = 1e6  # a bogus shift: would fail parity (and wrap) if the DMA read it later
+    got = g.get_coeffs()
+    ref = ref_in
+    for f in fields:
+        ref = oracle.round_layout(oracle.advect(ref, dims, k, 1, field=f, field_mask=1, n_double=n_double(precision, K)),
+                                  K, n_double(precision, K))
+    assert_parity(got, ref, K, precision, "host field clobbered after sldg_advect", ref_in, 1, k)
+    g.destroy()
