@@ -616,9 +616,8 @@ sldg_status advect_vnodes_impl(sldg_grid g, int dim, int vdim, const double* nod
         for (int64_t i = 0; i < n_entries; ++i)
             if (!(fabs(nodal[i]) < 4.611686018427387904e18))
                 return fail(SLDG_EINVAL, "non-finite or |nu| >= 2^62 entry in the nodal field");
-        sldg_status st = ensure_field(g, n_entries);
+        sldg_status st = upload_host_field(g, nodal, n_entries);  // copied before return (pinned ring)
         if (st != SLDG_OK) return st;
-        CU(cudaMemcpyAsync(g->d_field, nodal, n_entries * sizeof(double), cudaMemcpyHostToDevice, g->stream));
         dn = g->d_field;
     }
     const int64_t words = vnode_rec_words(L.k) * nv;
