@@ -124,7 +124,7 @@ __device__ __forceinline__ void vn_store(const Layout& L, const Arrays& a, int q
 }
 
 template <int KK>
-__global__ void __launch_bounds__(256) vnode_sweep_kernel(Layout lay, int d, int e, const double* __restrict__ rec,
+__global__ void __launch_bounds__(256, 3) vnode_sweep_kernel(Layout lay, int d, int e, const double* __restrict__ rec,
                                                          Arrays src, Arrays dst)
 {
     constexpr int K2 = KK * KK, K4 = K2 * K2;
