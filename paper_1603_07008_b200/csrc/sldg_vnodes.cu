@@ -123,8 +123,10 @@ __device__ __forceinline__ void vn_store(const Layout& L, const Arrays& a, int q
     else *fslot(a, lp, L.K, L.nd, q, L.L, inner) = __double2float_rn(v);
 }
 
+// 4 CTAs/SM for k <= 3, 3 for k = 4: the sweep waits on load latency, so resident warps pay
+// (profiles/round1/tuning.md, "Gauss-node x sweep")
 template <int KK>
-__global__ void __launch_bounds__(256, 3) vnode_sweep_kernel(Layout lay, int d, int e, const double* __restrict__ rec,
+__global__ void __launch_bounds__(256, KK <= 3 ? 4 : 3) vnode_sweep_kernel(Layout lay, int d, int e, const double* __restrict__ rec,
                                                          Arrays src, Arrays dst)
 {
     constexpr int K2 = KK * KK, K4 = K2 * K2;

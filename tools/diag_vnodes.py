@@ -15,7 +15,15 @@ hv = 12.0 / nv
 vc = -6.0 + (np.arange(nv) + 0.5) * hv
 nodal = ((vc[:, None] + xg[None, :] * hv / 2) * 0.05 / (4 * np.pi / dims[0])).reshape(-1)
 d = torch.tensor(nodal, dtype=torch.float64, device="cuda")
+import time
 for _ in range(5):
     g.advect_vnodes_device(0, vdim, d.data_ptr())
 g.sync()
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+if reps:
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        g.advect_vnodes_device(0, vdim, d.data_ptr())
+    g.sync()
+    print(f"{cfg} k={k}: {(time.perf_counter() - t0) / reps * 1e3:.3f} ms per nodal sweep (wall clock, incl. weights kernel)")
 print("ok")
