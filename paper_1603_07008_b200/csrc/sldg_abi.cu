@@ -373,6 +373,7 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
     const size_t need = 2 * tb + boff[P];
     if (g->t_bytes < need) {
         CU(cudaStreamSynchronize(g->stream));
+        tmap_cache_forget(g->t_alloc, g->t_bytes);
         cudaFree(g->t_alloc);
         g->t_alloc = nullptr;
         g->t_bytes = 0;
@@ -381,8 +382,12 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
     }
     char* tbase = (char*)g->t_alloc;
     const Arrays Tin = arrays_of(T, tbase), Tout = arrays_of(T, tbase + tb);
-    char* stage_fwd = (char*)g->alloc[1 - g->cur];  // dst array memory: overwritten by the unpack at the end
     char* stage_inv = tbase + 2 * tb;
+    // forward staging: the dst array's memory (overwritten by the unpack at the end) when the
+    // padded blocks fit in it; small shards whose 256-byte-aligned blocks do not fit share the
+    // inverse staging instead (the forward sends complete, stream-ordered, before the inverse
+    // receives land there)
+    char* stage_fwd = (boff[P] <= g->alloc_bytes) ? (char*)g->alloc[1 - g->cur] : stage_inv;
     auto bm = [&](char* base, int p) { return (double*)(base + boff[p]); };
     auto bf = [&](char* base, int p) {
         return (float*)(base + boff[p] + align256((size_t)(nl * nd * plan[p].send_slab_count * Mp) * 8));
@@ -718,6 +723,9 @@ sldg_status sldg_transpose_plan(int64_t n_outer, int64_t n_slab, int world, int 
 sldg_status sldg_advect_vnodes(sldg_grid g, int dim, int vdim, const double* nodal_nu)
 {
     if (!g) return fail(SLDG_EINVAL, "null grid");
+    // a captured graph would bake in one slot of the pinned staging ring (later host-field calls
+    // overwrite it) and a captured event that upload_host_field later synchronises on
+    if (g->capturing) return fail(SLDG_EINVAL, "host nodal field during graph capture: use sldg_advect_vnodes_device");
     return advect_vnodes_impl(g, dim, vdim, nodal_nu, false);
 }
 
@@ -892,7 +900,11 @@ sldg_status sldg_destroy(sldg_grid g)
     if (g->stream) cudaStreamSynchronize(g->stream);
     if (g->comm_stream) cudaStreamSynchronize(g->comm_stream);
     if (g->own_comm && g->comm) ncclCommDestroy((ncclComm_t)g->comm);
-    for (int b = 0; b < 2; ++b) cudaFree(g->alloc[b]);
+    for (int b = 0; b < 2; ++b) {
+        tmap_cache_forget(g->alloc[b], g->alloc_bytes);
+        cudaFree(g->alloc[b]);
+    }
+    tmap_cache_forget(g->t_alloc, g->t_bytes);
     cudaFree(g->w.shift);
     cudaFree(g->w.smod);
     cudaFree(g->w.copy);

@@ -198,6 +198,8 @@ cudaError_t launch_line(const Layout& lay, const Sweep& sw, const Arrays& src, c
 const char* line_kernel_name(const Layout& lay);
 cudaError_t launch_sweep_tma(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
                              int64_t layer_begin, int64_t layer_end, const TmaPlan& pl, cudaStream_t s);
+// drop cached tensor maps of buffers inside [base, base + bytes) (before that memory is freed)
+void tmap_cache_forget(const void* base, size_t bytes);
 
 }  // namespace sldg
 

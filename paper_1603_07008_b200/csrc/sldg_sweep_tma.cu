@@ -1354,31 +1354,59 @@ static bool build_tmaps(const Layout& lay, const Sweep& sw, const Arrays& src, c
 // small grids; the maps only depend on the source buffer, the layout and the plan, so they are
 // cached (two ping-pong buffers x D dims per grid; mutex-protected, handles may live on
 // different threads).
+// The key holds everything build_tmaps reads: the buffers, the device, the whole shape (two grids
+// with equal L and n[dim] but a different split of L into the dims below / above dim encode
+// different maps) and the plan.  sldg_destroy and the transpose path drop the entries of the
+// buffers they free (tmap_cache_forget), so a new allocation at a recycled address never hits.
 struct TmapCacheEntry {
     bool valid = false;
     const void* f = nullptr;
     const void* m = nullptr;
-    int dim = 0, W = 0, T = 0, Rmax = 0, R = 0, GC = 0;
+    int device = 0, prec = 0, D = 0, dim = 0, W = 0, T = 0, Rmax = 0, R = 0, GC = 0;
+    int64_t n[kMaxDim] = {};
     int64_t L = 0, layers = 0, pad = 0, nd = 0, K = 0;
     TmapSet maps;
 };
+static std::mutex g_tmap_mu;
+static TmapCacheEntry g_tmap_cache[32];
+static int g_tmap_next = 0;
+
+void tmap_cache_forget(const void* base, size_t bytes)
+{
+    if (!base) return;
+    const char* lo = (const char*)base;
+    const char* hi = lo + bytes;
+    std::lock_guard<std::mutex> lock(g_tmap_mu);
+    for (auto& e : g_tmap_cache) {
+        const char* f = (const char*)e.f;
+        const char* m = (const char*)e.m;
+        if (e.valid && ((f >= lo && f < hi) || (m >= lo && m < hi))) e.valid = false;
+    }
+}
+
+static bool same_shape(const TmapCacheEntry& e, const Layout& lay)
+{
+    if (e.D != lay.D || e.prec != lay.prec) return false;
+    for (int i = 0; i < kMaxDim; ++i)
+        if (e.n[i] != (i < lay.D ? lay.n[i] : 0)) return false;
+    return true;
+}
 
 static bool cached_tmaps(const Layout& lay, const Sweep& sw, const Arrays& src, const TmaPlan& pl, TmapSet* out)
 {
-    static std::mutex mu;
-    static TmapCacheEntry cache[32];
-    static int next = 0;
     const void* f = lay.prec == SLDG_FP64 ? (const void*)src.s64 : (const void*)src.pl;
-    std::lock_guard<std::mutex> lock(mu);
-    for (auto& e : cache)
-        if (e.valid && e.f == f && e.m == src.mass && e.dim == sw.dim && e.W == pl.W && e.T == pl.T &&
-            e.Rmax == pl.Rmax && e.R == pl.R && e.GC == pl.GC && e.L == lay.L && e.layers == lay.layers &&
-            e.pad == lay.pad && e.nd == sw.nd && e.K == lay.K) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_tmap_mu);
+    for (auto& e : g_tmap_cache)
+        if (e.valid && e.f == f && e.m == src.mass && e.device == dev && e.dim == sw.dim && e.W == pl.W &&
+            e.T == pl.T && e.Rmax == pl.Rmax && e.R == pl.R && e.GC == pl.GC && e.L == lay.L &&
+            e.layers == lay.layers && e.pad == lay.pad && e.nd == sw.nd && e.K == lay.K && same_shape(e, lay)) {
             *out = e.maps;
             return true;
         }
-    TmapCacheEntry& e = cache[next];
-    next = (next + 1) % 32;
+    TmapCacheEntry& e = g_tmap_cache[g_tmap_next];
+    g_tmap_next = (g_tmap_next + 1) % 32;
     memset(&e.maps, 0, sizeof(e.maps));
     if (!build_tmaps(lay, sw, src, pl, &e.maps)) {
         e.valid = false;
@@ -1387,6 +1415,10 @@ static bool cached_tmaps(const Layout& lay, const Sweep& sw, const Arrays& src, 
     e.valid = true;
     e.f = f;
     e.m = src.mass;
+    e.device = dev;
+    e.prec = lay.prec;
+    e.D = lay.D;
+    for (int i = 0; i < kMaxDim; ++i) e.n[i] = (i < lay.D) ? lay.n[i] : 0;
     e.dim = sw.dim;
     e.W = pl.W;
     e.T = pl.T;

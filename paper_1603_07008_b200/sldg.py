@@ -250,11 +250,19 @@ class Grid:
             _check(lib().sldg_advect(self.h, int(dim), float(shift), None, ctypes.c_uint32(field_mask)))
         else:
             f = np.ascontiguousarray(field, dtype=np.float64)
+            want = 1
+            for e in range(self.D):
+                if int(field_mask) >> e & 1:
+                    want *= self.cells[e]
+            if f.size != want:  # the C side reads exactly `want` doubles from this buffer
+                raise SldgError(SLDG_EINVAL, f"shift field has {f.size} entries, field_mask {field_mask:#x} needs {want}")
             _check(lib().sldg_advect(self.h, int(dim), float(shift), _dp(f), ctypes.c_uint32(field_mask)))
 
     def advect_vnodes(self, dim: int, vdim: int, nodal_nu):
         """x-sweep along dim with one CFL number per Gauss node of every v-cell of vdim (NEXT-3)."""
         f = np.ascontiguousarray(nodal_nu, dtype=np.float64)
+        if not 0 <= int(vdim) < self.D or f.size != self.cells[int(vdim)] * self.k:
+            raise SldgError(SLDG_EINVAL, f"nodal field has {f.size} entries, needs n[vdim] * k")
         _check(lib().sldg_advect_vnodes(self.h, int(dim), int(vdim), _dp(f)))
 
     def advect_vnodes_device(self, dim: int, vdim: int, d_nodal_ptr: int):

@@ -265,6 +265,49 @@ def test_mass_compensated_sum():
     assert abs(oracle.mass(c, 3, 0.25) - ref) <= 1e-15 * abs(ref) + 1e-9
 
 
+# ----------------------------------------------------------------------------- L2 norm
+def test_l2_norm_spec_constant_vs_zeros():
+    """S:94 worked example: a = constant 1 on [0,1], b = zeros -> 1.0 within 1e-13, any N."""
+    for N, k in [(1, 1), (7, 3), (64, 4), (33, 6)]:
+        a = np.zeros((N, k))
+        a[:, 0] = 1.0
+        assert abs(oracle.l2_norm_diff(a, np.zeros((N, k)), 1.0 / N, k) - 1.0) <= 1e-13
+        assert oracle.l2_norm_diff(a, a, 1.0 / N, k) == 0.0  # S:93 a = b -> 0
+
+
+def test_l2_norm_closed_forms_x_and_x2():
+    """Exact per-cell Legendre coefficients of x and x^2 on [0,1] (x = x_c + (h/2) xi,
+    xi^2 = P_0/3 + 2 P_2/3): ||x||_2 = 1/sqrt(3), ||x^2||_2 = 1/sqrt(5).  Exercises every
+    factor of S:90's formula: a dropped h, a dropped or wrong 1/(2j+1) changes the value."""
+    for N in (1, 2, 3, 10):
+        h = 1.0 / N
+        xc = (np.arange(N) + 0.5) * h
+        lin = np.zeros((N, 3))
+        lin[:, 0], lin[:, 1] = xc, h / 2
+        sq = np.zeros((N, 3))
+        sq[:, 0], sq[:, 1], sq[:, 2] = xc * xc + h * h / 12, xc * h, h * h / 6
+        z = np.zeros((N, 3))
+        assert abs(oracle.l2_norm_diff(lin, z, h, 3) - 1 / math.sqrt(3)) <= 1e-14
+        assert abs(oracle.l2_norm_diff(sq, z, h, 3) - 1 / math.sqrt(5)) <= 1e-14
+
+
+def test_l2_norm_node_formula_library():
+    """the node-based formula sqrt(sum_i (h/2) sum_q w_q (u_a - u_b)(x_iq)^2) with the
+    DG functions evaluated by numpy's Legendre series (library routines legval / leggauss)
+    agrees with the coefficient formula within 1e-12 on random grids."""
+    rng = np.random.default_rng(94)
+    for k in range(1, 8):
+        N = int(rng.integers(1, 40))
+        h = 2.5 / N
+        a, b = rng.standard_normal((N, k)), rng.standard_normal((N, k))
+        xq, wq = np.polynomial.legendre.leggauss(k + 1)
+        s = 0.0
+        for i in range(N):
+            du = np.polynomial.legendre.legval(xq, a[i] - b[i])
+            s += 0.5 * h * float(np.sum(wq * du * du))
+        assert abs(oracle.l2_norm_diff(a, b, h, k) - math.sqrt(s)) <= 1e-12 * max(1.0, math.sqrt(s))
+
+
 # ----------------------------------------------------------------------------- multi-D
 def _tensor(F, G, nF, kF):
     """c[cell, q] for cell = i0 + n0 * rest, q = m0 + k * qrest, from F[i0,m0] x G[rest,qrest]."""
