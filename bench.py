@@ -128,39 +128,111 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------------
 # CPU oracle (cpu_baseline leg and --impl reference): sampled lines of every sweep
 # ---------------------------------------------------------------------------------------------
-def oracle_sample(dims, kinds, k, precision, lines_per_sweep: int, seed: int = 1603):
-    """Time the CPU oracle on `lines_per_sweep` random lines of each sweep of the split step.
-    Returns (seconds, dofs).  Inputs are the parity generator's values for those cells."""
-    import oracle  # test infrastructure; only this leg of bench.py may use it
-
-    D, K = len(dims), k ** len(dims)
-    nd = 1 if precision == "mixed" else K
+def oracle_line_specs(dims, kinds, k, lines_per_sweep: int, seed: int = 1603, eps: float = 0.01):
+    """Random lines of every sweep of the split step: (sweep, dim, perpendicular cell base,
+    CFL number, input slot).  At most 64 distinct input lines per sweep are generated (the
+    oracle's time does not depend on the values); line i uses input slot i % 64."""
+    D = len(dims)
     lo, hi = domain(kinds)
     rng = np.random.default_rng(seed)
     S = np.cumprod([1] + list(dims[:-1]))
-    secs, dofs = 0.0, 0
-    n_inputs = 64  # distinct input lines generated per sweep (the oracle's time does not depend
-    for d, field, mask in sldg_inputs.vlasov_fields(dims, kinds, lo, hi):  # on the values)
+    specs = []
+    for si, (d, field, mask) in enumerate(sldg_inputs.vlasov_fields(dims, kinds, lo, hi, eps=eps)):
         fd = [e for e in range(D) if mask >> e & 1]
-        inputs = []
+        bases = {}
         for i in range(lines_per_sweep):
             perp = {e: int(rng.integers(0, dims[e])) for e in range(D) if e != d}
-            if i < n_inputs:
-                base = sum(perp[e] * S[e] for e in perp)
-                cells = base + np.arange(dims[d]) * S[d]
-                inputs.append(oracle.round_layout(sldg_inputs.random_coeffs(dims, k, seed, cells=cells), K, nd))
-            src = inputs[i % n_inputs]
             fi, st = 0, 1
             for e in fd:
                 fi += perp[e] * st
                 st *= dims[e]
-            ldims = [1] * D
-            ldims[d] = dims[d]
-            t0 = time.perf_counter()
-            oracle.advect(src, ldims, k, d, shift=float(field[fi]), n_double=nd)
-            secs += time.perf_counter() - t0
-            dofs += dims[d] * K
-    return secs, dofs
+            slot = i % 64
+            if slot not in bases:
+                bases[slot] = int(sum(perp[e] * S[e] for e in perp))
+            specs.append((si, d, bases[slot], float(field[fi]), slot))
+    return specs
+
+
+def oracle_run_specs(dims, k, precision, specs, seed: int = 1603):
+    """Run oracle.advect on each spec'd line (inputs: the parity generator's values of that
+    line).  Returns (timed seconds of the oracle calls only, DoF, per-line output digests)."""
+    import hashlib
+
+    import oracle  # test infrastructure; only the cpu_baseline / reference legs of bench.py use it
+
+    D, K = len(dims), k ** len(dims)
+    nd = 1 if precision == "mixed" else K
+    S = np.cumprod([1] + list(dims[:-1]))
+    cache = {}
+    secs, dofs, digests = 0.0, 0, []
+    for si, d, base, nu, slot in specs:
+        key = (si, slot)
+        if key not in cache:
+            cells = base + np.arange(dims[d]) * S[d]
+            cache[key] = oracle.round_layout(sldg_inputs.random_coeffs(dims, k, seed, cells=cells), K, nd)
+        ldims = [1] * D
+        ldims[d] = dims[d]
+        t0 = time.perf_counter()
+        out = oracle.advect(cache[key], ldims, k, d, shift=nu, n_double=nd)
+        secs += time.perf_counter() - t0
+        dofs += dims[d] * K
+        digests.append(hashlib.blake2b(out.tobytes(), digest_size=8).digest())
+    return secs, dofs, digests
+
+
+def _oracle_worker(a):
+    dims, k, precision, specs = a
+    return oracle_run_specs(dims, k, precision, specs)
+
+
+def host_cpu():
+    """nproc (the cores this process may use) and the CPU model (lscpu)."""
+    cores = len(os.sched_getaffinity(0))
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                model = ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    if model is None:
+        try:
+            with open("/proc/cpuinfo") as f:
+                model = next(ln.split(":", 1)[1].strip() for ln in f if ln.startswith("model name"))
+        except Exception:
+            model = "unknown"
+    return cores, model
+
+
+def oracle_baseline(dims, kinds, k, precision, lines_per_sweep: int, eps: float = 0.01):
+    """SURVEY 8(d) 'Timing the oracle': the same bounded sample of lines timed on 1 host core and
+    on all host cores (a process pool over independent lines; each line's result is
+    bit-identical to the 1-core leg's, checked by digest).  Throughput = DoF / oracle seconds
+    (1 core) and DoF / max over workers of their oracle seconds (all cores, concurrent)."""
+    import multiprocessing as mp
+    from concurrent.futures import ProcessPoolExecutor
+
+    specs = oracle_line_specs(dims, kinds, k, lines_per_sweep, eps=eps)
+    secs1, dofs, dig1 = oracle_run_specs(dims, k, precision, specs)
+    cores, model = host_cpu()
+    chunks = [specs[i::cores] for i in range(cores)]  # interleaved: every worker sees every sweep
+    with ProcessPoolExecutor(max_workers=cores, mp_context=mp.get_context("spawn")) as ex:
+        list(ex.map(_oracle_worker, [(dims, k, precision, c[:8]) for c in chunks]))  # start + warm workers
+        t0 = time.perf_counter()
+        res = list(ex.map(_oracle_worker, [(dims, k, precision, c) for c in chunks]))
+        wall = time.perf_counter() - t0
+    digp = [None] * len(specs)
+    for i, (_, _, dg) in enumerate(res):
+        digp[i::cores] = dg
+    secs_all = max(r[0] for r in res)
+    return {"value": dofs / secs1 / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "oracle",
+            "value_all_cores": dofs / secs_all / 1e9, "cores_all": cores,
+            "value_all_cores_wall": dofs / wall / 1e9,
+            "bit_identical_all_vs_1": digp == dig1, "cpu_model": model, "nproc": cores,
+            "sample": f"{lines_per_sweep} random lines per sweep x {len(dims)} sweeps of the same workload "
+                      f"({dofs} DoF; 1 core {secs1:.1f} s, {cores} cores {secs_all:.2f} s of oracle time per "
+                      f"worker, {wall:.2f} s wall incl. input generation); plain C oracle, -O2 -ffp-contract=off"}
 
 
 def run_reference(args, dims, kinds, k, cfg_json):
@@ -168,11 +240,11 @@ def run_reference(args, dims, kinds, k, cfg_json):
     if rank != 0:
         return 0
     lines = args.ref_lines
-    for _ in range(args.warmup):
-        oracle_sample(dims, kinds, k, args.precision, max(1, lines // 8))
+    for w in range(args.warmup):
+        oracle_run_specs(dims, k, args.precision, oracle_line_specs(dims, kinds, k, max(1, lines // 8), seed=99 + w))
     t_total, dof_total = 0.0, 0
     for s in range(args.steps):
-        t, n = oracle_sample(dims, kinds, k, args.precision, lines, seed=1603 + s)
+        t, n, _ = oracle_run_specs(dims, k, args.precision, oracle_line_specs(dims, kinds, k, lines, seed=1603 + s))
         t_total += t
         dof_total += n
     value = dof_total / t_total / 1e9
@@ -185,7 +257,8 @@ def run_reference(args, dims, kinds, k, cfg_json):
         "ms_per_step": t_total / args.steps * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfg_json,
         "hbm_gbs_equiv": value * bpd * 2,
-        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": 1, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GDoF/s", "cores": 1, "kind": "oracle", "sample": sample,
+                         "cpu_model": host_cpu()[1], "nproc": host_cpu()[0]},
         "e2e": {"value": value, "unit": "GDoF/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
@@ -193,6 +266,19 @@ def run_reference(args, dims, kinds, k, cfg_json):
 
 
 # ---------------------------------------------------------------------------------------------
+def self_launch(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: start N ranks (one process per GPU) with
+    torch.distributed.run on 127.0.0.1, exactly as the driver's torchrun command does."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -215,7 +301,17 @@ def main():
                     help="replay the timed steps from a CUDA graph of one split step (1 GPU)")
     ap.add_argument("--sweeps", default=None, help="comma list of dims to run (default: all)")
     ap.add_argument("--dims", default=None, help="override grid extents (profiling slabs), e.g. 128,128,128,16")
+    ap.add_argument("--force-halo", action="store_true",
+                    help="diagnostic: run the layer-dim sweep through the sharded halo path on one GPU")
+    ap.add_argument("--nccl-self", action="store_true",
+                    help="diagnostic (with --force-halo): the self halo through NCCL send/recv")
+    ap.add_argument("--timeline", action="store_true",
+                    help="record the device timeline of one step (sweeps + halo exchanges) into the JSON")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args.gpus)
+    if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={os.environ['WORLD_SIZE']}")
 
     dims, kinds, k0, desc = CONFIGS[args.config]
     if args.dims:
@@ -257,17 +353,22 @@ def main():
 
     lo, hi = domain(kinds)
     g = Grid(dims, k, lo=lo, hi=hi, precision=args.precision, rank=rank, world=world, unique_id=uid,
-             max_halo=2)
+             max_halo=2, force_halo=args.force_halo, nccl_self=args.nccl_self)
     terms = sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=args.eps)
     g.fill_separable(terms)
     sweeps = [s for s in sldg_inputs.vlasov_fields(dims, kinds, lo, hi, eps=args.eps) if s[0] in sweep_dims]
     dev_fields = [torch.tensor(f, dtype=torch.float64, device="cuda") for _, f, _ in sweeps]
+    bounds = [(float(np.min(f)), float(np.max(f))) for _, f, _ in sweeps]
     stream = torch.cuda.ExternalStream(g.stream())
     torch.cuda.synchronize()
+    sharded = world > 1 or args.force_halo
 
     def step():
-        for (d, _, m), tf in zip(sweeps, dev_fields):
-            g.advect_device(d, tf.data_ptr(), m)
+        for (d, _, m), tf, (b0, b1) in zip(sweeps, dev_fields, bounds):
+            if sharded:  # the field's bound sizes the halo on the host: no device -> host read
+                g.advect_device_bounded(d, tf.data_ptr(), m, b0, b1)
+            else:
+                g.advect_device(d, tf.data_ptr(), m)
 
     def barrier():
         if world > 1:
@@ -284,7 +385,7 @@ def main():
     # graph, else from the timed steps themselves
     # graphs only where the host's per-call cost shows (steps of < 1e9 DoF: C2-C4); C5's timed
     # region stays eager so the per-kernel events are taken inside it
-    use_graph = args.graph and world == 1 and len(sweeps) % 2 == 0 and len(sweeps) * cells * K < 1e9
+    use_graph = args.graph and len(sweeps) % 2 == 0 and len(sweeps) * cells * K / world < 1e9
     graph = None
     if use_graph:
         g.kernel_time(reset=True)
@@ -305,20 +406,25 @@ def main():
         g.kernel_time(reset=True)
         g.profile(True)
     launches0 = g.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # one event between consecutive steps (same stream, no host sync): per-step times for the
+    # median of the K repetitions (SURVEY 8(d) "median of >= 5 repetitions")
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    e0, e1 = evs[0], evs[-1]
     with ClockSampler(local_rank) as clk:
         barrier()
         with torch.cuda.stream(stream):
             e0.record(stream)
-        for _ in range(args.steps):
+        for i in range(args.steps):
             if graph is not None:
                 graph.launch()
             else:
                 step()
-        with torch.cuda.stream(stream):
-            e1.record(stream)
+            with torch.cuda.stream(stream):
+                evs[i + 1].record(stream)
         barrier()
     ms = e0.elapsed_time(e1)
+    step_times = torch.tensor([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)], dtype=torch.float64,
+                              device="cuda")
     launches = g.launch_count() - launches0
     if not use_graph:
         g.profile(False)
@@ -329,8 +435,19 @@ def main():
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(step_times, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
+    step_times = step_times.cpu().tolist()
     mass1 = g.mass()
+    timeline = None
+    if args.timeline:  # one eager step with every sweep launch and halo exchange on the device clock
+        g.profile(True)
+        g.timeline(reset=True)
+        step()
+        timeline = [{"kind": "halo" if kd < 0 else f"sweep dim {kd}", "t0_ms": a, "t1_ms": b}
+                    for kd, a, b in g.timeline(reset=True)]
+        g.profile(False)
+        g.kernel_time(reset=True)
 
     # ---------------------------------------------------------------- end-to-end (C ABI, host buffers)
     e2e = None
@@ -367,20 +484,18 @@ def main():
         dom = max(per_dim, key=lambda d: per_dim[d][0])
         d_ms, d_n, d_bytes = per_dim[dom]
         achieved = (d_bytes / d_n) / (d_ms / d_n * 1e-3) / 1e9 if d_n else None
-        traffic = None
+        traffic, traffic_all = None, None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_dram.json")) as f:
                 nd = json.load(f)
             key = f"{args.config}_{args.precision}_k{k}_dim{dom}"
             traffic = nd.get(key)
+            traffic_all = {str(d): nd.get(f"{args.config}_{args.precision}_k{k}_dim{d}") for d in sweep_dims}
         except Exception:
-            pass
+            traffic_all = None
         cpu = None
         if not args.no_cpu_baseline and world == 1:
-            secs, dofs = oracle_sample(dims, kinds, k, args.precision, args.cpu_lines)
-            cpu = {"value": dofs / secs / 1e9, "unit": "GDoF/s", "cores": 1, "kind": "oracle",
-                   "sample": f"{args.cpu_lines} random lines per sweep x {len(sweeps)} sweeps of the same "
-                             f"workload ({dofs} DoF, {secs:.1f} s of oracle time)"}
+            cpu = oracle_baseline(dims, kinds, k, args.precision, args.cpu_lines, eps=args.eps)
         out = {
             "metric": "GDoF/s per advection sweep (split step of all dims)",
             "value": value, "unit": "GDoF/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -391,6 +506,10 @@ def main():
             "hbm_frac_of_peak": alg_bytes_step / (step_ms * 1e-3) / 1e9 / world / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_per_sweep": traffic_all,
+                         "traffic_source": "profiles/ncu_dram.json: dram__bytes_read.sum + dram__bytes_write.sum "
+                                           "per launch of each sweep dim, ncu launch list of this config",
+                         "algorithmic_bytes_per_sweep": 2 * cells * bytes_per_cell(K, args.precision),
                          "kernel": f"{g.sweep_kernel(dom)} (sweep along dim {dom})",
                          "peak_source": peak_src,
                          "frac_of_spec_8000": (achieved / 8000.0) if achieved else None,
@@ -404,12 +523,19 @@ def main():
                        for d in per_dim},
             "kernel_share_of_step": (kt_all[0] / max(1, kt_all[1]) * len(sweeps) * args.steps) / ms if ms else None,
             "timed_steps": "CUDA graph of one split step, replayed" if use_graph else "eager calls",
+            "step_ms_median": statistics.median(step_times), "step_ms_min": min(step_times),
+            "step_ms_max": max(step_times),
+            "gdofs_median_step": dofs_per_step / (statistics.median(step_times) * 1e-3) / 1e9,
             "gpu_launches": launches,
             "mass_rel_drift": abs(mass1 - mass0) / abs(mass0),
             "clocks": clk.summary(),
             "e2e": e2e,
             "cpu_baseline": cpu,
         }
+        if timeline is not None:
+            out["timeline"] = timeline
+        if args.force_halo:
+            out["config"]["diagnostic"] = "forced halo path on one GPU" + (" (NCCL self)" if args.nccl_self else "")
     vp_res = None
     if args.vlasov and world == 1 and args.sweeps is None:
         vp_res = time_vlasov(g, stream, dims, kinds, k)

@@ -141,6 +141,16 @@ sldg_status sldg_advect(sldg_grid g, int dim, double shift, const double* field,
  * makes the next blocking call return EINVAL (sticky device error). */
 sldg_status sldg_advect_device(sldg_grid g, int dim, double shift, const double* d_field,
                                uint32_t field_mask);
+/* Same, with a caller-supplied bound: every entry of d_field lies in [nu_min, nu_max] (host
+ * doubles, finite, nu_min <= nu_max).  A sweep along the sharded dim then sizes its halo (and
+ * chooses halo or transpose) from the bound's integer parts floor(nu_min),
+ * floor(nu_max) instead of reading the field's range back to the host, so it never blocks and
+ * can be captured in a CUDA graph.  Entries outside the bound are found on the device: their
+ * lines are left unchanged and the next blocking call returns EINVAL (sticky device error),
+ * as for non-finite entries.  Errors: EINVAL (null field, bad bound, as sldg_advect_device).
+ * Asynchronous. */
+sldg_status sldg_advect_device_bounded(sldg_grid g, int dim, double shift, const double* d_field,
+                                       uint32_t field_mask, double nu_min, double nu_max);
 
 /* Gauss-node velocity treatment of an x-sweep (NEXT-3, reading V7): a sweep along
  * `dim` whose CFL number varies with the velocity coordinate of dim `vdim` INSIDE each v-cell.
@@ -186,6 +196,12 @@ sldg_status sldg_profile(sldg_grid g, int enable);
  * dims), their launch count, and the algorithmic bytes those launches moved (one load + one
  * store per stored coefficient).  Blocks.  reset != 0 clears all accumulators. */
 sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches, double* bytes, int reset);
+/* Profile mode: the device intervals (ms from the first recorded one) of every sweep launch
+ * (kinds[i] = its dim) and every halo exchange on the comm stream (kinds[i] = -1), in the order
+ * they were enqueued: 2 doubles per entry in t_ms.  Shows whether the interior sweep of a
+ * sharded sweep overlaps its halo exchange.  *n_out = number of recorded entries (up to
+ * max_entries are written); reset != 0 clears them.  Blocks. */
+sldg_status sldg_timeline(sldg_grid g, double* t_ms, int* kinds, int max_entries, int* n_out, int reset);
 /* Number of kernels this handle has launched (all kinds). */
 int64_t sldg_launch_count(sldg_grid g);
 /* Name of the sweep kernel a sweep along `dim` uses on this grid (static string; "" on bad
@@ -199,10 +215,13 @@ const char* sldg_sweep_kernel(sldg_grid g, int dim);
  * it with one launch: for small grids whose sweeps are shorter than the host's per-call cost.
  * Nothing runs during the capture.  A replay must start on the buffer the capture started on
  * (an odd number of sweeps flips the ping-pong buffer: capture two steps).  Device shift
- * fields must stay valid and are read at replay time.  Errors: EINVAL (capture already open /
- * not open, host field during capture, wrong current buffer at launch), ENOTSUP (sharded or
- * forced-halo grids: their layer-dim sweeps synchronise the host), ECUDA (a blocking call was
- * made inside the capture; the capture is then invalid). */
+ * fields must stay valid and are read at replay time.  Sharded grids: a device-field sweep
+ * along the sharded dim must use sldg_advect_device_bounded (its halo exchange, NCCL on the
+ * grid's comm stream, is captured with it), and a transpose-path sweep must have run once
+ * before (its buffers are allocated on first use).  Errors: EINVAL (capture already open /
+ * not open, host field during capture, unbounded device field along the sharded dim, wrong
+ * current buffer at launch), ECUDA (a blocking call was made inside the capture; the capture
+ * is then invalid). */
 typedef struct sldg_graph_s* sldg_graph;
 sldg_status sldg_graph_begin(sldg_grid g);
 sldg_status sldg_graph_end(sldg_grid g, sldg_graph* out);

@@ -89,6 +89,9 @@ size_t array_alloc_bytes(const Layout& L)
 sldg_status ensure_weights(sldg_grid g, int64_t n_entries)
 {
     if (g->w.cap >= n_entries) return SLDG_OK;
+    if (g->capturing)
+        return fail(SLDG_EINVAL, "the weight table grows on the first sweep with this many field entries: run the "
+                                 "sequence once before capturing it");
     g->w_const = false;
     cudaFree(g->w.shift);
     cudaFree(g->w.smod);
@@ -110,6 +113,7 @@ sldg_status ensure_weights(sldg_grid g, int64_t n_entries)
 sldg_status ensure_field(sldg_grid g, int64_t n)
 {
     if (g->field_cap >= n) return SLDG_OK;
+    if (g->capturing) return fail(SLDG_EINVAL, "the field buffer grows on first use: run the sequence once before capturing it");
     cudaFree(g->d_field);
     g->d_field = nullptr;
     g->field_cap = 0;
@@ -194,9 +198,13 @@ sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arr
     const Layout& LY = lay ? *lay : g->lay;
     if (le <= lb) return SLDG_OK;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEvent_t t0 = nullptr, t1 = nullptr;  // timeline copies (sldg_timeline owns them)
     if (g->profile) {
         e0 = pool_event(g);
         e1 = pool_event(g);
+        t0 = pool_event(g);
+        t1 = pool_event(g);
+        CU(cudaEventRecord(t0, g->stream));
         CU(cudaEventRecord(e0, g->stream));
     }
     int nl = 0;
@@ -204,9 +212,12 @@ sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arr
     g->launches += nl;
     if (g->profile) {
         CU(cudaEventRecord(e1, g->stream));
+        CU(cudaEventRecord(t1, g->stream));
         g->ev_pairs.push_back({e0, e1});
         g->ev_bytes.push_back(2.0 * (double)bytes_per_cell(LY) * (double)((le - lb) * LY.L));
         g->ev_dim.push_back(sw.dim);
+        g->tl_ev.push_back({t0, t1});
+        g->tl_kind.push_back(sw.dim);
     }
     return SLDG_OK;
 }
@@ -371,6 +382,9 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
         boff[p + 1] = boff[p] + align256((size_t)(nl * nd * len) * 8) + align256((size_t)(nl * nf * len) * 4);
     }
     const size_t need = 2 * tb + boff[P];
+    if (g->t_bytes < need && g->capturing)
+        return fail(SLDG_EINVAL, "the transpose path's buffers grow on its first use: run the sequence once "
+                                 "before capturing it");
     if (g->t_bytes < need) {
         CU(cudaStreamSynchronize(g->stream));
         tmap_cache_forget(g->t_alloc, g->t_bytes);
@@ -438,6 +452,9 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
         }
         const double* fT = nullptr;
         if (dfield) {
+            if (g->tfield_cap < n_T && g->capturing)
+                return fail(SLDG_EINVAL, "the transpose path's field buffer grows on its first use: run the "
+                                         "sequence once before capturing it");
             if (g->tfield_cap < n_T) {
                 CU(cudaStreamSynchronize(st));
                 cudaFree(g->d_tfield);
@@ -494,8 +511,10 @@ sldg_status transpose_sweep(sldg_grid g, Sweep sw, const double* dfield, double 
     return SLDG_OK;
 }
 
+// bounded: the caller guarantees every field entry lies in [nu_lo, nu_hi] (sldg_advect_device_bounded);
+// the halo plan is sized from that bound instead of a device -> host read of the field's range
 sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field, bool field_on_device,
-                        uint32_t mask)
+                        uint32_t mask, bool bounded = false, double nu_lo = 0.0, double nu_hi = 0.0)
 {
     const Layout& L = g->lay;
     if (dim < 0 || dim >= L.D) return fail(SLDG_EINVAL, "dim out of range");
@@ -520,7 +539,23 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
     }
     const bool sharded_sweep = (g->halo_mode && dim == L.D - 1);
     int64_t imin = 0, imax = 0;
-    if (!field) {
+    int64_t ilo = INT64_MIN, ihi = INT64_MAX;  // device-checked bound of the field's i*
+    auto int_part = [](double nu) {
+        const double fl = floor(nu);
+        return (int64_t)fl + ((nu - fl >= 1.0) ? 1 : 0);
+    };
+    if (bounded) {
+        if (!field) return fail(SLDG_EINVAL, "a shift bound needs a field");
+        if (!(fabs(nu_lo) < 4.611686018427387904e18) || !(fabs(nu_hi) < 4.611686018427387904e18) || nu_lo > nu_hi)
+            return fail(SLDG_EINVAL, "shift bound must be finite with nu_min <= nu_max");
+        ilo = imin = int_part(nu_lo);
+        ihi = imax = int_part(nu_hi);
+    }
+    if (sharded_sweep && field && field_on_device && !bounded && g->capturing)
+        return fail(SLDG_EINVAL, "a device-field sweep along the sharded dim inside a graph capture needs a shift "
+                                 "bound (sldg_advect_device_bounded): its halo is sized on the host");
+    if (bounded) {
+    } else if (!field) {
         if (!(fabs(shift) < 4.611686018427387904e18)) return fail(SLDG_EINVAL, "non-finite or huge shift");
         double fl = floor(shift);
         imin = imax = (int64_t)fl + ((shift - fl >= 1.0) ? 1 : 0);
@@ -549,7 +584,7 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
             dfield = g->d_field;
         }
     }
-    if (sharded_sweep && field && field_on_device) {
+    if (sharded_sweep && field && field_on_device && !bounded) {
         CU(launch_field_range(dfield, n_entries, shift, g->d_range, g->stream));
         int64_t r[2];
         CU(cudaMemcpyAsync(r, g->d_range, sizeof(r), cudaMemcpyDeviceToHost, g->stream));
@@ -559,7 +594,7 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
         if (imin > imax) imin = imax = 0;  // all entries invalid: lines are copied (error sticky)
     }
     if (field || !g->w_const || g->w_shift != shift || g->w_n != sw.nd) {
-        CU(launch_weights(L, sw.nd, dfield, shift, n_entries, g->w, g->d_err, g->stream));
+        CU(launch_weights(L, sw.nd, dfield, shift, n_entries, g->w, g->d_err, g->stream, ilo, ihi));
         g->launches += 1;
         g->w_const = !field;
         g->w_shift = shift;
@@ -590,12 +625,27 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
         sw.wrap = 0;
         CU(cudaEventRecord(g->ev_ready, g->stream));
         CU(cudaStreamWaitEvent(g->comm_stream, g->ev_ready, 0));
+        cudaEvent_t h0 = nullptr, h1 = nullptr;
+        if (g->profile) {
+            h0 = pool_event(g);
+            h1 = pool_event(g);
+            CU(cudaEventRecord(h0, g->comm_stream));
+        }
         st = halo_exchange(g, src, left, right);
         if (st != SLDG_OK) return st;
+        if (g->profile) {
+            CU(cudaEventRecord(h1, g->comm_stream));
+            g->tl_ev.push_back({h0, h1});
+            g->tl_kind.push_back(-1);
+        }
         CU(cudaEventRecord(g->ev_halo, g->comm_stream));
-        // interior layers need no halo: overlap them with the exchange
+        // interior layers need no halo: overlap them with the exchange, leaving comm_sms SMs to
+        // the NCCL kernel (a persistent sweep CTA and an NCCL CTA do not fit one SM together)
         int64_t ib = std::min(left, L.layers), ie = std::max(ib, L.layers - right);
-        st = run_sweep(g, sw, src, dst, ib, ie);
+        const bool exchange = (P > 1 || g->nccl_self) && (left + right) > 0;
+        Sweep swi = sw;
+        swi.sm_reserve = exchange ? g->comm_sms : 0;
+        st = run_sweep(g, swi, src, dst, ib, ie);
         if (st != SLDG_OK) return st;
         CU(cudaStreamWaitEvent(g->stream, g->ev_halo, 0));
         st = run_sweep(g, sw, src, dst, 0, ib);
@@ -849,6 +899,11 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
         cudaEventCreateWithFlags(&g->ev_ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventCreateWithFlags(&g->ev_halo, cudaEventDisableTiming) != cudaSuccess)
         return bail(fail(SLDG_ECUDA, "stream/event create failed"));
+    if (const char* e = getenv("SLDG_COMM_SMS")) g->comm_sms = std::max(0, atoi(e));  // tuning override
+    {  // the minimum weight table (constant shifts): such sweeps never allocate, also inside a capture
+        sldg_status ws = ensure_weights(g, 1);
+        if (ws != SLDG_OK) return bail(ws);
+    }
     g->alloc_bytes = array_alloc_bytes(L);
     for (int b = 0; b < 2; ++b) {
         cudaError_t e = cudaMalloc(&g->alloc[b], g->alloc_bytes);
@@ -928,6 +983,10 @@ sldg_status sldg_destroy(sldg_grid g)
         cudaEventDestroy(p.first);
         cudaEventDestroy(p.second);
     }
+    for (auto& p : g->tl_ev) {
+        cudaEventDestroy(p.first);
+        cudaEventDestroy(p.second);
+    }
     for (auto e : g->ev_pool) cudaEventDestroy(e);
     if (g->ev_ready) cudaEventDestroy(g->ev_ready);
     if (g->ev_halo) cudaEventDestroy(g->ev_halo);
@@ -1004,7 +1063,6 @@ sldg_status sldg_graph_begin(sldg_grid g)
 {
     if (!g) return fail(SLDG_EINVAL, "null grid");
     if (g->capturing) return fail(SLDG_EINVAL, "a capture is already open");
-    if (g->halo_mode) return fail(SLDG_ENOTSUP, "graph capture of a sharded grid (halo sweeps sync the host)");
     CU(cudaStreamBeginCapture(g->stream, cudaStreamCaptureModeThreadLocal));
     g->capturing = true;
     g->cap_cur = g->cur;
@@ -1069,6 +1127,42 @@ sldg_status sldg_graph_destroy(sldg_graph gr)
     if (gr->g) cudaStreamSynchronize(gr->g->stream);
     if (gr->exec) cudaGraphExecDestroy(gr->exec);
     delete gr;
+    return SLDG_OK;
+}
+
+sldg_status sldg_advect_device_bounded(sldg_grid g, int dim, double shift, const double* d_field,
+                                       uint32_t field_mask, double nu_min, double nu_max)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    if (!d_field) return fail(SLDG_EINVAL, "null device field");
+    return advect_impl(g, dim, shift, d_field, true, field_mask, true, nu_min, nu_max);
+}
+
+sldg_status sldg_timeline(sldg_grid g, double* t_ms, int* kinds, int max_entries, int* n_out, int reset)
+{
+    if (!g || !n_out || (max_entries > 0 && (!t_ms || !kinds))) return fail(SLDG_EINVAL, "null argument");
+    CU(cudaStreamSynchronize(g->stream));
+    CU(cudaStreamSynchronize(g->comm_stream));
+    const int n = (int)g->tl_ev.size();
+    *n_out = n;
+    if (n == 0) return SLDG_OK;
+    cudaEvent_t origin = g->tl_ev[0].first;  // the first recorded interval starts at 0
+    for (int i = 0; i < n && i < max_entries; ++i) {
+        float a = 0.f, b = 0.f;
+        CU(cudaEventElapsedTime(&a, origin, g->tl_ev[i].first));
+        CU(cudaEventElapsedTime(&b, origin, g->tl_ev[i].second));
+        t_ms[2 * i] = a;
+        t_ms[2 * i + 1] = b;
+        kinds[i] = g->tl_kind[i];
+    }
+    if (reset) {
+        for (auto& pr : g->tl_ev) {
+            g->ev_pool.push_back(pr.first);
+            g->ev_pool.push_back(pr.second);
+        }
+        g->tl_ev.clear();
+        g->tl_kind.clear();
+    }
     return SLDG_OK;
 }
 

@@ -83,6 +83,8 @@ struct Sweep {
     const int* copy;
     const double* ab;
     const double* rec;     // packed line records (see Weights::rec)
+    int sm_reserve = 0;    // persistent TMA kernels: leave this many SMs free (a concurrent halo
+                           // exchange's NCCL kernel cannot co-reside with a ~200 KB-smem CTA)
 };
 
 struct Grid {
@@ -145,8 +147,11 @@ struct GaussTab {
 const GaussTab& gauss_table(int k);
 
 // ---- kernel launchers (sldg_kernels.cu) -------------------------------------------------
+// [ilo, ihi]: integer-shift bound of the field (sldg_advect_device_bounded); an entry outside
+// it (or non-finite) leaves its lines unchanged and raises the sticky device error
 cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field, double shift,
-                           int64_t n_entries, Weights& w, int* d_err, cudaStream_t s);
+                           int64_t n_entries, Weights& w, int* d_err, cudaStream_t s,
+                           int64_t ilo = INT64_MIN, int64_t ihi = INT64_MAX);
 cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst,
                          int64_t layer_begin, int64_t layer_end, cudaStream_t s, int* n_launched);
 cudaError_t launch_mass_partials(const Layout& lay, const Arrays& a, double* d_partials,
@@ -216,6 +221,11 @@ struct sldg_grid_s : public sldg::Grid {
     double* d_tfield = nullptr;    // transpose path: the field restricted to this rank's slab
     int64_t tfield_cap = 0;
     int64_t transposes = 0;        // sweeps that took the transpose path
+    int comm_sms = 8;              // SMs the interior sweep leaves to the concurrent halo exchange
+    // profile mode: device intervals of halo exchanges (comm stream) and of every profiled sweep
+    // launch, for the overlap timeline (sldg_timeline)
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tl_ev;
+    std::vector<int> tl_kind;      // sweep dim, or -1 for a halo exchange
     double* d_vnrec = nullptr;     // Gauss-node sweep: per-v-cell operator records
     int64_t vnrec_cap = 0;
     // graph capture (sldg_graph_begin/end)

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(32) build_weights_kernel(int64_t nd, const dou
                                      int64_t n_entries, int64_t* __restrict__ sh_raw,
                                      int64_t* __restrict__ sh_mod, int* __restrict__ cpy,
                                      double* __restrict__ ab, double* __restrict__ rec, int* __restrict__ err,
-                                     const GaussTab gt)
+                                     const GaussTab gt, int64_t ilo, int64_t ihi)
 {
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_entries) return;
@@ -59,6 +59,11 @@ __global__ void __launch_bounds__(32) build_weights_kernel(int64_t nd, const dou
         is = (int64_t)fl;
         if (a >= 1.0) {  // tiny negative nu: alpha rounds to 1 (reading R2)
             is += 1;
+            a = 0.0;
+        }
+        if (is < ilo || is > ihi) {  // outside the caller's bound: the halo may not cover it
+            atomicExch(err, 1);
+            is = 0;
             a = 0.0;
         }
     }
@@ -139,7 +144,7 @@ const GaussTab& gauss_table(int k)
 }
 
 cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field, double shift,
-                           int64_t n_entries, Weights& w, int* d_err, cudaStream_t s)
+                           int64_t n_entries, Weights& w, int* d_err, cudaStream_t s, int64_t ilo, int64_t ihi)
 {
     // small blocks: one entry per thread is a serial fp64 build, so spread entries over SMs
     int threads = 32;
@@ -147,7 +152,7 @@ cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field,
     const GaussTab& gt = gauss_table(lay.k);
 #define SLDG_W(KK)                                                                                           \
     build_weights_kernel<KK><<<(unsigned)blocks, threads, 0, s>>>(nd, d_field, shift, n_entries, w.shift, w.smod, \
-                                                                  w.copy, w.ab, w.rec, d_err, gt)
+                                                                  w.copy, w.ab, w.rec, d_err, gt, ilo, ihi)
     switch (lay.k) {
         case 1: SLDG_W(1); break;
         case 2: SLDG_W(2); break;

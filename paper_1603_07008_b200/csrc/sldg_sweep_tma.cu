@@ -1451,7 +1451,7 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
             attr_set[pl.ctas] = true;
         }
-        int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
+        int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, g_num_sms - sw.sm_reserve) * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
     } else if constexpr (KK <= 6) {
@@ -1469,7 +1469,7 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
             attr_set[pl.ctas][pl.pspan] = true;
         }
-        int64_t grid = std::min<int64_t>(ntiles, (int64_t)g_num_sms * per_sm);
+        int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, g_num_sms - sw.sm_reserve) * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
     } else {

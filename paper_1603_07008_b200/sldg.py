@@ -23,7 +23,7 @@ STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "E
 # every symbol include/sldg.h declares
 EXPORTS = [
     "sldg_create", "sldg_create_ex", "sldg_destroy", "sldg_set_coeffs", "sldg_get_coeffs", "sldg_advect",
-    "sldg_advect_device", "sldg_mass", "sldg_shard_info", "sldg_sync", "sldg_set_stream",
+    "sldg_advect_device", "sldg_advect_device_bounded", "sldg_timeline", "sldg_mass", "sldg_shard_info", "sldg_sync", "sldg_set_stream",
     "sldg_get_stream", "sldg_memory_bytes", "sldg_last_error", "sldg_fill_random",
     "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
     "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_halo_plan", "sldg_layer_owner",
@@ -80,6 +80,10 @@ def lib():
         "sldg_get_coeffs": [vp, dp, i64, i64],
         "sldg_advect": [vp, ctypes.c_int, ctypes.c_double, dp, u32],
         "sldg_advect_device": [vp, ctypes.c_int, ctypes.c_double, vp, u32],
+        "sldg_advect_device_bounded": [vp, ctypes.c_int, ctypes.c_double, vp, u32, ctypes.c_double,
+                                       ctypes.c_double],
+        "sldg_timeline": [vp, dp, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                          ctypes.c_int],
         "sldg_mass": [vp, dp],
         "sldg_shard_info": [vp, i64p, i64p],
         "sldg_sync": [vp],
@@ -271,6 +275,22 @@ class Grid:
     def advect_device(self, dim: int, d_field_ptr: int, field_mask: int, shift: float = 0.0):
         _check(lib().sldg_advect_device(self.h, int(dim), float(shift), ctypes.c_void_p(d_field_ptr),
                                         ctypes.c_uint32(field_mask)))
+
+    def advect_device_bounded(self, dim: int, d_field_ptr: int, field_mask: int, nu_min: float, nu_max: float,
+                              shift: float = 0.0):
+        """advect_device with a caller bound nu_min <= every entry <= nu_max: a sharded sweep sizes
+        its halo from the bound (no host synchronisation; graph-capturable)."""
+        _check(lib().sldg_advect_device_bounded(self.h, int(dim), float(shift), ctypes.c_void_p(d_field_ptr),
+                                                ctypes.c_uint32(field_mask), float(nu_min), float(nu_max)))
+
+    def timeline(self, reset: bool = True):
+        """[(kind, t0_ms, t1_ms)] of the profiled sweeps (kind = dim) and halo exchanges (-1)."""
+        n = ctypes.c_int()
+        _check(lib().sldg_timeline(self.h, None, None, 0, ctypes.byref(n), 0))
+        t = np.zeros(2 * max(1, n.value))
+        kinds = (ctypes.c_int * max(1, n.value))()
+        _check(lib().sldg_timeline(self.h, _dp(t), kinds, n.value, ctypes.byref(n), int(reset)))
+        return [(int(kinds[i]), float(t[2 * i]), float(t[2 * i + 1])) for i in range(n.value)]
 
     def mass(self) -> float:
         m = ctypes.c_double()
