@@ -305,6 +305,8 @@ def main():
                     help="diagnostic: run the layer-dim sweep through the sharded halo path on one GPU")
     ap.add_argument("--nccl-self", action="store_true",
                     help="diagnostic (with --force-halo): the self halo through NCCL send/recv")
+    ap.add_argument("--fuse-x", action=argparse.BooleanOptionalAction, default=False,
+                    help="run the dim-0 and dim-1 sweeps as one fused pass (sldg_advect_pair_device, NEXT-4)")
     ap.add_argument("--timeline", action="store_true",
                     help="record the device timeline of one step (sweeps + halo exchanges) into the JSON")
     args = ap.parse_args()
@@ -363,8 +365,14 @@ def main():
     torch.cuda.synchronize()
     sharded = world > 1 or args.force_halo
 
+    fuse = args.fuse_x and len(sweeps) >= 2 and sweeps[0][0] == 0 and sweeps[1][0] == 1
+
     def step():
-        for (d, _, m), tf, (b0, b1) in zip(sweeps, dev_fields, bounds):
+        first = 0
+        if fuse:  # x1 + x2 in one pass over HBM (sldg_advect_pair_device)
+            g.advect_pair_device(dev_fields[0].data_ptr(), sweeps[0][2], dev_fields[1].data_ptr(), sweeps[1][2])
+            first = 2
+        for (d, _, m), tf, (b0, b1) in list(zip(sweeps, dev_fields, bounds))[first:]:
             if sharded:  # the field's bound sizes the halo on the host: no device -> host read
                 g.advect_device_bounded(d, tf.data_ptr(), m, b0, b1)
             else:
@@ -396,6 +404,9 @@ def main():
         g.profile(False)
         kt_all = g.kernel_time(-1)
         per_dim = {d: g.kernel_time(d) for d in sweep_dims}
+        if fuse:
+            per_dim = {d: v for d, v in per_dim.items() if v[1] > 0}
+            per_dim[-2] = g.kernel_time(-2)
         g.graph_begin()
         step()
         graph = g.graph_end()
@@ -430,6 +441,9 @@ def main():
         g.profile(False)
         kt_all = g.kernel_time(-1)
         per_dim = {d: g.kernel_time(d) for d in sweep_dims}
+        if fuse:
+            per_dim = {d: v for d, v in per_dim.items() if v[1] > 0}
+            per_dim[-2] = g.kernel_time(-2)
     if graph is not None:
         graph.destroy()
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -461,7 +475,11 @@ def main():
         barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            for (d, _, m), p in zip(sweeps, pinned):
+            first = 0
+            if fuse:
+                g.advect_pair(0.0, pinned[0].numpy(), sweeps[0][2], 0.0, pinned[1].numpy(), sweeps[1][2])
+                first = 2
+            for (d, _, m), p in list(zip(sweeps, pinned))[first:]:
                 g.advect(d, field=p.numpy(), field_mask=m)
             g.mass()  # D2H read of the step's diagnostic (blocking)
         barrier()
@@ -488,7 +506,7 @@ def main():
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_dram.json")) as f:
                 nd = json.load(f)
-            key = f"{args.config}_{args.precision}_k{k}_dim{dom}"
+            key = f"{args.config}_{args.precision}_k{k}_dim{dom}" if dom >= 0 else f"{args.config}_{args.precision}_k{k}_fused01"
             traffic = nd.get(key)
             traffic_all = {str(d): nd.get(f"{args.config}_{args.precision}_k{k}_dim{d}") for d in sweep_dims}
         except Exception:
@@ -510,7 +528,8 @@ def main():
                          "traffic_source": "profiles/ncu_dram.json: dram__bytes_read.sum + dram__bytes_write.sum "
                                            "per launch of each sweep dim, ncu launch list of this config",
                          "algorithmic_bytes_per_sweep": 2 * cells * bytes_per_cell(K, args.precision),
-                         "kernel": f"{g.sweep_kernel(dom)} (sweep along dim {dom})",
+                         "kernel": (f"{g.sweep_kernel(dom)} (sweep along dim {dom})" if dom >= 0 else
+                                    "sweep_fused01_kernel (dims 0 + 1 in one pass: bytes of ONE read + write)"),
                          "peak_source": peak_src,
                          "frac_of_spec_8000": (achieved / 8000.0) if achieved else None,
                          "bytes_per_launch": d_bytes / d_n if d_n else None,
@@ -518,7 +537,8 @@ def main():
                                            "graph-replayed timed region") if use_graph else
                                           "CUDA events around each sweep launch inside the timed region",
                          "avg_launch_ms": d_ms / d_n if d_n else None},
-            "sweeps": {str(d): {"ms_per_launch": per_dim[d][0] / max(1, per_dim[d][1]),
+            "fused_x": fuse,
+            "sweeps": {(str(d) if d >= 0 else "fused01"): {"ms_per_launch": per_dim[d][0] / max(1, per_dim[d][1]),
                                 "gbs": (per_dim[d][2] / (per_dim[d][0] * 1e-3) / 1e9) if per_dim[d][0] else None}
                        for d in per_dim},
             "kernel_share_of_step": (kt_all[0] / max(1, kt_all[1]) * len(sweeps) * args.steps) / ms if ms else None,

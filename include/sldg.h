@@ -152,6 +152,21 @@ sldg_status sldg_advect_device(sldg_grid g, int dim, double shift, const double*
 sldg_status sldg_advect_device_bounded(sldg_grid g, int dim, double shift, const double* d_field,
                                        uint32_t field_mask, double nu_min, double nu_max);
 
+/* Two sweeps of a split step: along dim 0 with (shift0, field0, mask0), then along dim 1 with
+ * (shift1, field1, mask1) -- exactly sldg_advect(g, 0, ...) followed by sldg_advect(g, 1, ...)
+ * (P:144-149 dimension splitting, each sweep P:259-272), including the intermediate rounded to
+ * the storage precision.  When both fields are constant over dims 0 and 1 (they depend only on
+ * dims >= 2, as the x1 / x2 CFL numbers v1, v2 of the 4D Vlasov workload) and D >= 3,
+ * 32 <= n_0 <= 256 with 256 % n_0 == 0, k <= 3, the pair runs as ONE pass over HBM (one read
+ * and one write of every stored coefficient for both sweeps), with results bit
+ * for bit those of the two sweeps; otherwise as the two sweeps.  Fields: HOST memory
+ * (sldg_advect_pair; copied before return) or DEVICE memory (_device; validated on the device as
+ * in sldg_advect_device).  Errors: EINVAL as sldg_advect.  Asynchronous. */
+sldg_status sldg_advect_pair(sldg_grid g, double shift0, const double* field0, uint32_t mask0, double shift1,
+                             const double* field1, uint32_t mask1);
+sldg_status sldg_advect_pair_device(sldg_grid g, double shift0, const double* d_field0, uint32_t mask0,
+                                    double shift1, const double* d_field1, uint32_t mask1);
+
 /* Gauss-node velocity treatment of an x-sweep (NEXT-3, reading V7): a sweep along
  * `dim` whose CFL number varies with the velocity coordinate of dim `vdim` INSIDE each v-cell.
  * Per v-cell j: modal -> nodal in vdim at the k Gauss-Legendre nodes, one SLDG line
@@ -193,11 +208,13 @@ sldg_status sldg_fill_separable(sldg_grid g, int n_terms, const double* tables);
 /* When enabled, CUDA events bracket every sweep kernel on the handle's stream. */
 sldg_status sldg_profile(sldg_grid g, int enable);
 /* Sum of sweep-kernel durations (ms) since the last reset for sweeps along `dim` (-1: all
- * dims), their launch count, and the algorithmic bytes those launches moved (one load + one
- * store per stored coefficient).  Blocks.  reset != 0 clears all accumulators. */
+ * dims and fused pairs, -2: fused sweep pairs only), their launch count, and the algorithmic
+ * bytes those launches moved (one load + one store per stored coefficient; a fused
+ * pair counts its single pass).  Blocks.  reset != 0 clears all accumulators. */
 sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches, double* bytes, int reset);
 /* Profile mode: the device intervals (ms from the first recorded one) of every sweep launch
- * (kinds[i] = its dim) and every halo exchange on the comm stream (kinds[i] = -1), in the order
+ * (kinds[i] = its dim; -2 for a fused sweep pair) and every halo exchange on the comm stream
+ * (kinds[i] = -1), in the order
  * they were enqueued: 2 doubles per entry in t_ms.  Shows whether the interior sweep of a
  * sharded sweep overlaps its halo exchange.  *n_out = number of recorded entries (up to
  * max_entries are written); reset != 0 clears them.  Blocks. */

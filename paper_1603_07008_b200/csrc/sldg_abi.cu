@@ -86,27 +86,28 @@ size_t array_alloc_bytes(const Layout& L)
     return ((rows * 8 * (size_t)L.nd + 255) / 256) * 256 + rows * 4 * (size_t)(L.K - L.nd);
 }
 
-sldg_status ensure_weights(sldg_grid g, int64_t n_entries)
+sldg_status ensure_weights(sldg_grid g, int64_t n_entries, Weights* wp = nullptr)
 {
-    if (g->w.cap >= n_entries) return SLDG_OK;
+    Weights& w = wp ? *wp : g->w;
+    if (w.cap >= n_entries) return SLDG_OK;
     if (g->capturing)
         return fail(SLDG_EINVAL, "the weight table grows on the first sweep with this many field entries: run the "
                                  "sequence once before capturing it");
-    g->w_const = false;
-    cudaFree(g->w.shift);
-    cudaFree(g->w.smod);
-    cudaFree(g->w.copy);
-    cudaFree(g->w.ab);
-    cudaFree(g->w.rec);
-    g->w = Weights{};
+    if (&w == &g->w) g->w_const = false;
+    cudaFree(w.shift);
+    cudaFree(w.smod);
+    cudaFree(w.copy);
+    cudaFree(w.ab);
+    cudaFree(w.rec);
+    w = Weights{};
     int64_t cap = std::max<int64_t>(n_entries, 64);
     const int k = g->lay.k;
-    CU(cudaMalloc(&g->w.shift, cap * sizeof(int64_t)));
-    CU(cudaMalloc(&g->w.smod, cap * sizeof(int64_t)));
-    CU(cudaMalloc(&g->w.copy, cap * sizeof(int)));
-    CU(cudaMalloc(&g->w.ab, cap * 2 * k * k * sizeof(double)));
-    CU(cudaMalloc(&g->w.rec, cap * (2 * k * k + 2) * sizeof(double)));
-    g->w.cap = cap;
+    CU(cudaMalloc(&w.shift, cap * sizeof(int64_t)));
+    CU(cudaMalloc(&w.smod, cap * sizeof(int64_t)));
+    CU(cudaMalloc(&w.copy, cap * sizeof(int)));
+    CU(cudaMalloc(&w.ab, cap * 2 * k * k * sizeof(double)));
+    CU(cudaMalloc(&w.rec, cap * (2 * k * k + 2) * sizeof(double)));
+    w.cap = cap;
     return SLDG_OK;
 }
 
@@ -657,6 +658,125 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
     return SLDG_OK;
 }
 
+// sldg_advect_pair: the dim-0 sweep then the dim-1 sweep, in one pass when fused_plan accepts
+// the shapes and fields (sldg_fused.cu), else as the two sweeps.
+sldg_status advect_pair_impl(sldg_grid g, double shift0, const double* f0, uint32_t m0, double shift1,
+                             const double* f1, uint32_t m1, bool on_device)
+{
+    const Layout& L = g->lay;
+    if (L.D < 2) return fail(SLDG_EINVAL, "a sweep pair needs dims 0 and 1");
+    auto make_sweep = [&](int dim, const double* f, uint32_t mask, int64_t* n_entries) -> sldg_status {
+        if (mask >> L.D) return fail(SLDG_EINVAL, "field_mask has bits >= ndim");
+        if (f && (mask & (1u << dim))) return fail(SLDG_EINVAL, "field_mask contains the advected dim");
+        if (!f && mask) return fail(SLDG_EINVAL, "field_mask given without a field");
+        *n_entries = 1;
+        for (int e = 0; e < L.D; ++e)
+            if (f && (mask >> e & 1u)) *n_entries *= L.n[e];
+        return SLDG_OK;
+    };
+    int64_t ne0 = 1, ne1 = 1;
+    sldg_status st = make_sweep(0, f0, m0, &ne0);
+    if (st != SLDG_OK) return st;
+    st = make_sweep(1, f1, m1, &ne1);
+    if (st != SLDG_OK) return st;
+    auto sweep_of = [&](int dim, const double* f, uint32_t mask) {
+        Sweep sw{};
+        sw.dim = dim;
+        sw.nd = L.n[dim];
+        sw.fmask = f ? mask : 0;
+        sw.wrap = 1;
+        int64_t stv = 1;
+        for (int e = 0; e < kMaxDim; ++e) {
+            sw.fstride[e] = 0;
+            if (e < L.D && (sw.fmask >> e & 1u)) {
+                sw.fstride[e] = stv;
+                stv *= L.n[e];
+            }
+        }
+        return sw;
+    };
+    if (!on_device && g->capturing && (f0 || f1))
+        return fail(SLDG_EINVAL, "a host shift field cannot be captured in a graph: use sldg_advect_pair_device");
+    Sweep s0 = sweep_of(0, f0, m0), s1 = sweep_of(1, f1, m1);
+    FusedPlan fp;
+    // dim 1 must not be the sharded layer dim (D >= 3); both fields constant over dims 0, 1
+    const bool fuse = L.D >= 3 && fused_plan(L, s0, s1, &fp);
+    if (!fuse) {
+        st = advect_impl(g, 0, shift0, f0, on_device, m0);
+        if (st != SLDG_OK) return st;
+        return advect_impl(g, 1, shift1, f1, on_device, m1);
+    }
+    if (!on_device) {
+        for (int pass = 0; pass < 2; ++pass) {
+            const double* f = pass ? f1 : f0;
+            const int64_t n = pass ? ne1 : ne0;
+            const double sh = pass ? shift1 : shift0;
+            if (!f) {
+                if (!(fabs(sh) < 4.611686018427387904e18)) return fail(SLDG_EINVAL, "non-finite or huge shift");
+                continue;
+            }
+            for (int64_t e = 0; e < n; ++e)
+                if (!(fabs(f[e]) < 4.611686018427387904e18))
+                    return fail(SLDG_EINVAL, "non-finite or |nu| >= 2^62 entry in shift field");
+        }
+    }
+    st = ensure_weights(g, ne0);
+    if (st != SLDG_OK) return st;
+    st = ensure_weights(g, ne1, &g->w2);
+    if (st != SLDG_OK) return st;
+    // weights of each sweep (a host field goes through the pinned staging ring, stream-ordered
+    // before its weight build)
+    const double* d0 = f0;
+    if (f0 && !on_device) {
+        st = upload_host_field(g, f0, ne0);
+        if (st != SLDG_OK) return st;
+        d0 = g->d_field;
+    }
+    CU(launch_weights(L, L.n[0], d0, shift0, ne0, g->w, g->d_err, g->stream));
+    g->launches += 1;
+    g->w_const = false;
+    const double* d1 = f1;
+    if (f1 && !on_device) {
+        st = upload_host_field(g, f1, ne1);
+        if (st != SLDG_OK) return st;
+        d1 = g->d_field;
+    }
+    CU(launch_weights(L, L.n[1], d1, shift1, ne1, g->w2, g->d_err, g->stream));
+    g->launches += 1;
+    s0.shift = g->w.shift;
+    s0.smod = g->w.smod;
+    s0.copy = g->w.copy;
+    s0.ab = g->w.ab;
+    s0.rec = g->w.rec;
+    s1.shift = g->w2.shift;
+    s1.smod = g->w2.smod;
+    s1.copy = g->w2.copy;
+    s1.ab = g->w2.ab;
+    s1.rec = g->w2.rec;
+    cudaEvent_t e0 = nullptr, e1 = nullptr, t0 = nullptr, t1 = nullptr;
+    if (g->profile) {
+        e0 = pool_event(g);
+        e1 = pool_event(g);
+        t0 = pool_event(g);
+        t1 = pool_event(g);
+        CU(cudaEventRecord(t0, g->stream));
+        CU(cudaEventRecord(e0, g->stream));
+    }
+    CU(launch_fused01(L, s0, s1, g->buf[g->cur], g->buf[1 - g->cur], fp, g->stream));
+    g->launches += 1;
+    if (g->profile) {
+        CU(cudaEventRecord(e1, g->stream));
+        CU(cudaEventRecord(t1, g->stream));
+        g->ev_pairs.push_back({e0, e1});
+        g->ev_bytes.push_back(2.0 * (double)bytes_per_cell(L) * (double)L.cells);  // ONE read + write: two sweeps
+        g->ev_dim.push_back(kMaxDim);
+        g->tl_ev.push_back({t0, t1});
+        g->tl_kind.push_back(-2);
+    }
+    g->cur = 1 - g->cur;
+    return SLDG_OK;
+}
+
 sldg_status advect_vnodes_impl(sldg_grid g, int dim, int vdim, const double* nodal, bool on_device)
 {
     const Layout& L = g->lay;
@@ -957,9 +1077,15 @@ sldg_status sldg_destroy(sldg_grid g)
     if (g->own_comm && g->comm) ncclCommDestroy((ncclComm_t)g->comm);
     for (int b = 0; b < 2; ++b) {
         tmap_cache_forget(g->alloc[b], g->alloc_bytes);
+        fused_cache_forget(g->alloc[b], g->alloc_bytes);
         cudaFree(g->alloc[b]);
     }
     tmap_cache_forget(g->t_alloc, g->t_bytes);
+    cudaFree(g->w2.shift);
+    cudaFree(g->w2.smod);
+    cudaFree(g->w2.copy);
+    cudaFree(g->w2.ab);
+    cudaFree(g->w2.rec);
     cudaFree(g->w.shift);
     cudaFree(g->w.smod);
     cudaFree(g->w.copy);
@@ -1138,6 +1264,20 @@ sldg_status sldg_advect_device_bounded(sldg_grid g, int dim, double shift, const
     return advect_impl(g, dim, shift, d_field, true, field_mask, true, nu_min, nu_max);
 }
 
+sldg_status sldg_advect_pair(sldg_grid g, double shift0, const double* field0, uint32_t mask0, double shift1,
+                             const double* field1, uint32_t mask1)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    return advect_pair_impl(g, shift0, field0, mask0, shift1, field1, mask1, false);
+}
+
+sldg_status sldg_advect_pair_device(sldg_grid g, double shift0, const double* d_field0, uint32_t mask0, double shift1,
+                                    const double* d_field1, uint32_t mask1)
+{
+    if (!g) return fail(SLDG_EINVAL, "null grid");
+    return advect_pair_impl(g, shift0, d_field0, mask0, shift1, d_field1, mask1, true);
+}
+
 sldg_status sldg_timeline(sldg_grid g, double* t_ms, int* kinds, int max_entries, int* n_out, int reset)
 {
     if (!g || !n_out || (max_entries > 0 && (!t_ms || !kinds))) return fail(SLDG_EINVAL, "null argument");
@@ -1275,7 +1415,7 @@ sldg_status sldg_profile(sldg_grid g, int enable)
 sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches, double* bytes, int reset)
 {
     if (!g) return fail(SLDG_EINVAL, "null grid");
-    if (dim < -1 || dim >= g->lay.D) return fail(SLDG_EINVAL, "dim out of range");
+    if (dim < -2 || dim >= g->lay.D) return fail(SLDG_EINVAL, "dim out of range");
     CU(cudaStreamSynchronize(g->stream));
     for (size_t i = 0; i < g->ev_pairs.size(); ++i) {
         float t = 0.f;
@@ -1292,8 +1432,10 @@ sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches
     g->ev_dim.clear();
     double m = 0.0, b = 0.0;
     int64_t n = 0;
-    for (int d = 0; d < g->lay.D; ++d) {
+    for (int d = 0; d <= kMaxDim; ++d) {
+        if (d >= g->lay.D && d != kMaxDim) continue;
         if (dim >= 0 && d != dim) continue;
+        if (dim == -2 && d != kMaxDim) continue;  // -2: fused sweep pairs only
         m += g->prof_ms[d];
         b += g->prof_bytes[d];
         n += g->prof_launches[d];
@@ -1302,7 +1444,7 @@ sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches
     if (launches) *launches = n;
     if (bytes) *bytes = b;
     if (reset) {
-        for (int d = 0; d < kMaxDim; ++d) {
+        for (int d = 0; d <= kMaxDim; ++d) {
             g->prof_ms[d] = 0.0;
             g->prof_bytes[d] = 0.0;
             g->prof_launches[d] = 0;

@@ -1,0 +1,498 @@
+// sldg_fused.cu -- the dim-0 and dim-1 sweeps of a split step in ONE pass over HBM (SURVEY 8(f)
+// NEXT-4 "multi-sweep fusion").
+//
+// sldg_advect_pair = sldg_advect(dim 0, field0) followed by sldg_advect(dim 1, field1) (P:144-149
+// dimension splitting; each sweep the two-cell update of P:259-272).  When both CFL fields are
+// constant over dims 0 and 1 (they depend only on dims >= 2: the x1/x2 sweeps of the 4D Vlasov
+// workload, whose CFL numbers are v1 / v2), every (dims >= 2) slab sees one shift per sweep,
+// and the pair is evaluated slab by slab from shared memory:
+//
+//   x1(r, i0)      = A1 c(r, i0 - i1* - 1) + B1 c(r, i0 - i1*)            (row r of the slab)
+//   out(t, i0)     = A2 x1(t - i2* - 1, i0) + B2 x1(t - i2*, i0)
+//
+// with x1 rounded to the storage precision exactly as the stored intermediate of the two-sweep
+// path would be, and the same FMA order as the sweep kernels (x1: A- and B-parts as two chains,
+// then one add, as sweep_d0_tma; out: the A-part carried from the previous row, then the B terms,
+// as sweep_strided_tma), so the fused result is the two-sweep result bit for bit.  HBM traffic:
+// one read and one write of every stored coefficient for the two sweeps (half of two passes).
+//
+// Kernel: persistent, 8 consumer warps + 1 TMA producer warp (the sweep_strided_tma pattern).
+// A tile = NS = 256 / n0 slabs ("lanes", one consumer thread per (lane, i0) column) x one coupled
+// group of the pair (the k^2 slots (m0, m1) at fixed m2..m_{D-1}); the consumers walk the slab's
+// n1 rows in stages of Tsub rows, carrying the x2 A-part across stages, so only the first stage
+// of a line loads the extra (prologue) row.  Stage rows arrive as one box per plane and per run of
+// rows (a run ends where the rows wrap around the periodic line), each run as boxes of 2^h rows.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "sldg_internal.h"
+#include "sldg_ptx.cuh"
+
+namespace sldg {
+
+// A stage holds, per lane, a run of h <= RA consecutive source rows of the group's k^2 planes as
+// ONE box (the mixed mass group: its fp64 mass plane + its k^2 - 1 fp32 planes), landing slot-major
+// ([slot][h rows][n0]).  A lane's line is the cyclic row sequence R_k = (R_0 + k) mod n1,
+// k = 0..n1, R_0 = -i2* - 1 (k = 0: the prologue row, the A-source of target 0; k >= 1: the
+// B-source of target k - 1); it is cut into runs at every RA rows and at the wrap n1 - 1 -> 0, so
+// no box wraps.  Every lane of a tile takes the same number of stages (empty runs pad the lanes
+// whose line has no wrap inside).
+constexpr int kFzMaxRows = 8;
+struct FusedMaps {
+    CUtensorMap fA[kFzMaxRows];   // {n0, h rows, 1, k^2 planes}: fp32 planes (mixed) or all slots (fp64)
+    CUtensorMap fA1[kFzMaxRows];  // mixed mass group: {n0, h, 1, k^2 - 1} fp32 planes
+    CUtensorMap mA[kFzMaxRows];   // mixed: {n0, h, 1, 1} of the fp64 mass array
+};
+
+// run `st` of a lane whose line starts at row R0: first sequence index k0, rows h (0: empty), row
+__host__ __device__ __forceinline__ void fz_run(int n1, int RA, int R0, int st, int* k0, int* h, int* row)
+{
+    const int kw = n1 - R0;               // first k whose row wraps to 0 (1 <= kw <= n1)
+    const int na = (kw + RA - 1) / RA;    // runs before the wrap
+    if (st < na) {
+        *k0 = st * RA;
+        *h = (kw - *k0) < RA ? (kw - *k0) : RA;
+    } else {
+        *k0 = kw + (st - na) * RA;
+        const int left = n1 + 1 - *k0;
+        *h = left <= 0 ? 0 : (left < RA ? left : RA);
+    }
+    const int r = R0 + *k0;
+    *row = r >= n1 ? r - n1 : r;
+}
+
+// field entry of a slab (dims >= 2; s = i_mid + M_mid * local layer)
+__device__ __forceinline__ int64_t fz_field(const Sweep& sw, const Layout& lay, int64_t s, int64_t M_mid)
+{
+    int64_t im = s % M_mid, l = s / M_mid, f = 0;
+    for (int e = 2; e < lay.D - 1; ++e) {
+        f += (im % lay.n[e]) * sw.fstride[e];
+        im /= lay.n[e];
+    }
+    return f + (lay.first_layer + l) * sw.fstride[lay.D - 1];
+}
+
+// one consumer thread's line state: weights of both sweeps, source columns, the carried A-part
+template <int KK>
+struct FzLine {
+    double A1[KK * KK], B1[KK * KK], A2[KK * KK], B2[KK * KK];
+    double sA[KK * KK];
+    int ca = 0, cb = 0, cp0 = 0, cp1 = 0, R0 = 0;
+    double* o64 = nullptr;  // output slot 0 of the group at (i0 = c, i1 = 0)
+    float* o32 = nullptr;   // output fp32 plane of slot 0 (mixed; slot j at + j L)
+};
+
+// The h rows of a run (sequence indices k0 ..): x1 of each row (rounded to storage, as the
+// stored intermediate of the two-sweep path), then the x2 update of target k - 1 (k >= 1) and
+// the carried A-part.  CPY: some sweep of this line has alpha = 0 (exact copies, R4).
+template <int KK, int PREC, bool MASSG, bool CPY>
+__device__ __forceinline__ void fz_rows(FzLine<KK>& ln, const unsigned char* lbase, int h, int n0, int k0, int64_t L)
+{
+    constexpr int K2 = KK * KK;
+    constexpr int E = (PREC == SLDG_FP64) ? 8 : 4;
+    const int pb = h * n0 * E;                                          // bytes per (non-mass) slot
+    const int mshift = (MASSG && PREC == SLDG_MIXED) ? h * n0 * 4 : 0;  // the fp64 mass slot is wider
+#pragma unroll 1
+    for (int r = 0; r < h; ++r) {
+        const int ea = r * n0 + ln.ca, eb = r * n0 + ln.cb;
+        double x1[K2];
+#pragma unroll
+        for (int m1 = 0; m1 < KK; ++m1) {
+            double va[KK], vb[KK];
+#pragma unroll
+            for (int m0 = 0; m0 < KK; ++m0) {
+                const int j = m0 + KK * m1;
+                const bool dbl = PREC == SLDG_FP64 || (MASSG && j == 0);
+                const unsigned char* p = lbase + j * pb + (j > 0 ? mshift : 0);
+                if (dbl) {
+                    va[m0] = ((const double*)p)[ea];
+                    vb[m0] = ((const double*)p)[eb];
+                } else {
+                    va[m0] = (double)((const float*)p)[ea];
+                    vb[m0] = (double)((const float*)p)[eb];
+                }
+            }
+#pragma unroll
+            for (int m0 = 0; m0 < KK; ++m0) {
+                const int j = m0 + KK * m1;
+                const bool dbl = PREC == SLDG_FP64 || (MASSG && j == 0);
+                double v;
+                if (CPY && ln.cp0) {
+                    v = vb[m0];  // alpha = 0: exact copy (R4)
+                } else {
+                    // A- and B-parts as two chains, then one add (sweep_d0_tma's order)
+                    double oa = 0.0, ob = 0.0;
+#pragma unroll
+                    for (int l = 0; l < KK; ++l) {
+                        oa = fma(ln.A1[m0 * KK + l], va[l], oa);
+                        ob = fma(ln.B1[m0 * KK + l], vb[l], ob);
+                    }
+                    v = oa + ob;
+                }
+                x1[j] = dbl ? v : (double)__double2float_rn(v);  // the stored intermediate
+            }
+        }
+        const int k = k0 + r;
+        if (k > 0) {
+            const int64_t off = (int64_t)n0 * (k - 1);
+#pragma unroll
+            for (int m0 = 0; m0 < KK; ++m0) {
+#pragma unroll
+                for (int m1o = 0; m1o < KK; ++m1o) {
+                    const int j = m0 + KK * m1o;
+                    double o;
+                    if (CPY && ln.cp1) {
+                        o = x1[j];  // alpha = 0: exact copy of the B-source (R4)
+                    } else {
+                        o = ln.sA[j];  // the carried A-part, then the B terms (sweep_strided_tma's order)
+#pragma unroll
+                        for (int m1 = 0; m1 < KK; ++m1) o = fma(ln.B2[m1o * KK + m1], x1[m0 + KK * m1], o);
+                    }
+                    if (PREC == SLDG_FP64)
+                        __stcs(ln.o64 + off + (int64_t)j * L, o);
+                    else if (MASSG && j == 0)
+                        __stcs(ln.o64 + off, o);
+                    else
+                        __stcs(ln.o32 + off + (int64_t)j * L, __double2float_rn(o));
+                }
+            }
+        }
+#pragma unroll
+        for (int m0 = 0; m0 < KK; ++m0)
+#pragma unroll
+            for (int m1o = 0; m1o < KK; ++m1o) {
+                double a = 0.0;
+#pragma unroll
+                for (int m1 = 0; m1 < KK; ++m1) a = fma(ln.A2[m1o * KK + m1], x1[m0 + KK * m1], a);
+                ln.sA[m0 + KK * m1o] = a;
+            }
+    }
+}
+
+template <int KK, int PREC>
+__global__ void __launch_bounds__(kTmaThreads, 1)
+    sweep_fused01_kernel(Layout lay, Sweep s0, Sweep s1, Arrays dst, FusedPlan fp, const __grid_constant__ FusedMaps maps)
+{
+    constexpr int K2 = KK * KK;
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int S = fp.stages;
+    uint64_t* full = (uint64_t*)smem;
+    uint64_t* empty = full + S;
+    unsigned char* stage0 = smem + 256;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    constexpr int NC = kTmaConsumerWarps;
+    const bool producer = (warp == NC);
+    const int n0 = (int)lay.n[0], n1 = (int)lay.n[1];
+    const int NS = fp.NS, RA = fp.rows_alloc;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC);
+        }
+        fence_barrier_init();
+        for (int h = 0; h < RA; ++h) {
+            prefetch_tmap(&maps.fA[h]);
+            if (PREC == SLDG_MIXED) {
+                prefetch_tmap(&maps.fA1[h]);
+                prefetch_tmap(&maps.mA[h]);
+            }
+        }
+    }
+    __syncthreads();
+
+    const int G = lay.K / K2;
+    const int64_t M_mid = fp.M_mid;
+    const int64_t ntiles = ((fp.nslab + NS - 1) / NS) * G;
+    const int nst = (n1 + 1 + RA - 1) / RA + 1;  // runs per lane line (the wrap may add one)
+    const uint64_t pol_in = policy_evict_normal();
+    auto cell_bytes = [&](bool mg) { return (PREC == SLDG_FP64) ? 8 * K2 : 4 * K2 + (mg ? 4 : 0); };
+
+    uint32_t it = 0;
+    if (producer) {
+        if (lane == 0) {
+            for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                const int gq = (int)(tile % G);
+                const int64_t sg = tile / G;
+                const bool massg = (PREC == SLDG_MIXED) && gq == 0;
+                int R0[8], lmid[8], llay[8];
+                int nl = 0;
+                for (int b = 0; b < NS; ++b) {
+                    const int64_t sl = sg * NS + b;
+                    if (sl >= fp.nslab) break;
+                    const int i2s = (int)__ldg(&s1.smod[fz_field(s1, lay, sl, M_mid)]);
+                    R0[b] = (n1 - i2s - 1) % n1;
+                    lmid[b] = (int)(sl % M_mid);
+                    llay[b] = (int)(sl / M_mid);
+                    ++nl;
+                }
+                for (int st = 0; st < nst; ++st) {
+                    const int s = it % S;
+                    const uint32_t ph = (it / S) & 1;
+                    ++it;
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint32_t bytes = 0;
+                    int hh[8], rr[8];
+                    for (int b = 0; b < nl; ++b) {
+                        int k0;
+                        fz_run(n1, RA, R0[b], st, &k0, &hh[b], &rr[b]);
+                        bytes += (uint32_t)(hh[b] * n0 * cell_bytes(massg));
+                    }
+                    mbar_expect_tx(&full[s], bytes);
+                    unsigned char* stp = stage0 + (size_t)s * fp.stage_bytes;
+                    for (int b = 0; b < nl; ++b) {
+                        if (hh[b] == 0) continue;
+                        unsigned char* lb = stp + (size_t)b * fp.lane_bytes;
+                        const int h = hh[b] - 1, c4 = (int)(lay.pad + llay[b]), q0 = gq * K2;
+                        if (massg) {
+                            tma_5d(lb, &maps.mA[h], 0, rr[b], lmid[b], 0, c4, &full[s], pol_in);
+                            tma_5d(lb + hh[b] * n0 * 8, &maps.fA1[h], 0, rr[b], lmid[b], 0, c4, &full[s], pol_in);
+                        } else {
+                            tma_5d(lb, &maps.fA[h], 0, rr[b], lmid[b], (PREC == SLDG_FP64) ? q0 : q0 - 1, c4, &full[s],
+                                   pol_in);
+                        }
+                    }
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers: thread = (lane b, column c) ----
+    const int tid = threadIdx.x;
+    const int b = tid / n0, c = tid % n0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int gq = (int)(tile % G);
+        const int64_t sg = tile / G;
+        const bool massg = (PREC == SLDG_MIXED) && gq == 0;
+        const int64_t sl = sg * NS + b;
+        const bool active = (b < NS) && (sl < fp.nslab);
+        FzLine<KK> ln;
+        if (active) {
+            const int64_t f0 = fz_field(s0, lay, sl, M_mid), f1 = fz_field(s1, lay, sl, M_mid);
+#pragma unroll
+            for (int i = 0; i < K2; ++i) {
+                ln.A1[i] = __ldg(&s0.ab[f0 * 2 * K2 + i]);
+                ln.B1[i] = __ldg(&s0.ab[f0 * 2 * K2 + K2 + i]);
+                ln.A2[i] = __ldg(&s1.ab[f1 * 2 * K2 + i]);
+                ln.B2[i] = __ldg(&s1.ab[f1 * 2 * K2 + K2 + i]);
+            }
+            const int i1s = (int)__ldg(&s0.smod[f0]);
+            const int i2s = (int)__ldg(&s1.smod[f1]);
+            ln.R0 = (n1 - i2s - 1) % n1;
+            ln.cp0 = __ldg(&s0.copy[f0]);
+            ln.cp1 = __ldg(&s1.copy[f1]);
+            ln.cb = c - i1s;
+            if (ln.cb < 0) ln.cb += n0;
+            ln.ca = ln.cb == 0 ? n0 - 1 : ln.cb - 1;
+            const int64_t layerp = lay.pad + sl / M_mid;
+            const int64_t inner0 = c + (int64_t)n0 * n1 * (sl % M_mid);
+            // slot q = gq k^2 + j: fp32 plane q - 1 (mixed) / slot q (fp64) of layer layerp
+            ln.o64 = (PREC == SLDG_FP64) ? dst.s64 + (layerp * lay.K + (int64_t)gq * K2) * lay.L + inner0
+                                         : dst.mass + layerp * lay.L + inner0;
+            ln.o32 = dst.pl + (layerp * (lay.K - 1) + (int64_t)gq * K2 - 1) * lay.L + inner0;
+        }
+#pragma unroll
+        for (int i = 0; i < K2; ++i) ln.sA[i] = 0.0;
+        const bool cpy = ln.cp0 || ln.cp1;
+        for (int st = 0; st < nst; ++st) {
+            const int s = it % S;
+            const uint32_t ph = (it / S) & 1;
+            ++it;
+            mbar_wait(&full[s], ph);
+            if (active) {
+                int k0, h, row;
+                fz_run(n1, RA, ln.R0, st, &k0, &h, &row);
+                if (h > 0) {
+                    const unsigned char* lbase = stage0 + (size_t)s * fp.stage_bytes + (size_t)b * fp.lane_bytes;
+                    if (massg) {
+                        if (cpy) fz_rows<KK, PREC, true, true>(ln, lbase, h, n0, k0, lay.L);
+                        else fz_rows<KK, PREC, true, false>(ln, lbase, h, n0, k0, lay.L);
+                    } else {
+                        if (cpy) fz_rows<KK, PREC, false, true>(ln, lbase, h, n0, k0, lay.L);
+                        else fz_rows<KK, PREC, false, false>(ln, lbase, h, n0, k0, lay.L);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+    }
+}
+
+// ============================================================================================
+// host: plan, tensor maps, launch
+// ============================================================================================
+bool fused_plan(const Layout& lay, const Sweep& s0, const Sweep& s1, FusedPlan* fp)
+{
+    *fp = FusedPlan{};
+    if (getenv("SLDG_FUSED") && atoi(getenv("SLDG_FUSED")) == 0) return false;  // A/B override
+    if (lay.D < 3 || lay.prec == SLDG_GENERAL || lay.k > 3 || lay.k < 1) return false;
+    // both fields constant over dims 0 and 1 (one shift per slab and sweep)
+    if ((s0.fmask & 3u) || (s1.fmask & 3u)) return false;
+    const int64_t n0 = lay.n[0], n1 = lay.n[1];
+    if (n0 < 32 || n0 > 256 || 256 % n0 != 0 || n1 < 2) return false;
+    int sms = 0, optin = 0;
+    tma_device_info(&sms, &optin);
+    if (!sms) return false;
+    const int k = lay.k, K2 = k * k;
+    const int64_t M_mid = lay.L / (n0 * n1);
+    const int64_t layers_alloc = lay.layers + 2 * lay.pad;
+    if (lay.L > ((int64_t)1 << 31) || layers_alloc > 65535 || M_mid > 65535) return false;
+    fp->NS = (int)(256 / n0);
+    fp->M_mid = M_mid;
+    fp->nslab = M_mid * lay.layers;
+    const int cell = (lay.prec == SLDG_FP64) ? 8 * K2 : 8 + 4 * (K2 - 1);  // bytes per cell of a group (max)
+    const int64_t budget = std::min<int64_t>(optin, 200 * 1024) - 256;
+    int stages = 3;
+    if (const char* e = getenv("SLDG_FUSED_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
+    int64_t ra = budget / stages / (256LL * cell);
+    if (const char* e = getenv("SLDG_FUSED_TSUB")) ra = std::min<int64_t>(ra, atoi(e) + 1);
+    ra = std::min<int64_t>(ra, std::min<int64_t>(n1 + 1, kFzMaxRows));
+    if (ra < 2) return false;
+    fp->rows_alloc = (int)ra;
+    fp->Tsub = (int)ra - 1;
+    fp->lane_bytes = (int)((ra * n0 * cell + 127) / 128 * 128);
+    fp->stage_bytes = fp->lane_bytes * fp->NS;
+    fp->stages = stages;
+    return true;
+}
+
+static bool build_fused_maps(const Layout& lay, const Arrays& src, const FusedPlan& fp, FusedMaps* m)
+{
+    const bool f64 = lay.prec == SLDG_FP64;
+    const int64_t P = f64 ? lay.K : lay.K - 1;
+    const int64_t n0 = lay.n[0], n1 = lay.n[1], L = lay.L;
+    const int64_t layers_alloc = lay.layers + 2 * lay.pad;
+    const int K2 = lay.k * lay.k;
+    void* fbase = f64 ? (void*)src.s64 : (void*)src.pl;
+    const int64_t dm[5] = {n0, n1, fp.M_mid, P, layers_alloc};
+    const int64_t sm[5] = {1, n0, n0 * n1, L, L * P};
+    const int64_t dmm[5] = {n0, n1, fp.M_mid, 1, layers_alloc};
+    const int64_t smm[5] = {1, n0, n0 * n1, L, L};
+    for (int h = 1; h <= fp.rows_alloc; ++h) {  // one family per run height
+        const int bA[5] = {(int)n0, h, 1, K2, 1};
+        if (!make_tmap5(&m->fA[h - 1], f64, fbase, dm, sm, bA)) return false;
+        if (!f64) {
+            const int bA1[5] = {(int)n0, h, 1, K2 - 1, 1};
+            const int bm[5] = {(int)n0, h, 1, 1, 1};
+            if (!make_tmap5(&m->fA1[h - 1], false, fbase, dm, sm, bA1) ||
+                !make_tmap5(&m->mA[h - 1], true, src.mass, dmm, smm, bm))
+                return false;
+        }
+    }
+    return true;
+}
+
+// maps per source buffer and shape (two ping-pong buffers per grid); dropped with the buffers
+struct FzCacheEntry {
+    bool valid = false;
+    const void* f = nullptr;
+    const void* m = nullptr;
+    int device = 0, prec = 0, D = 0;
+    int64_t n[kMaxDim] = {};
+    int64_t layers = 0, pad = 0;
+    int ra = 0;
+    FusedMaps maps;
+};
+static std::mutex g_fz_mu;
+static FzCacheEntry g_fz_cache[8];
+static int g_fz_next = 0;
+
+void fused_cache_forget(const void* base, size_t bytes)
+{
+    if (!base) return;
+    const char* lo = (const char*)base;
+    const char* hi = lo + bytes;
+    std::lock_guard<std::mutex> lock(g_fz_mu);
+    for (auto& e : g_fz_cache) {
+        const char* f = (const char*)e.f;
+        const char* m = (const char*)e.m;
+        if (e.valid && ((f >= lo && f < hi) || (m >= lo && m < hi))) e.valid = false;
+    }
+}
+
+static bool cached_fused_maps(const Layout& lay, const Arrays& src, const FusedPlan& fp, FusedMaps* out)
+{
+    const void* f = lay.prec == SLDG_FP64 ? (const void*)src.s64 : (const void*)src.pl;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(g_fz_mu);
+    for (auto& e : g_fz_cache) {
+        if (!e.valid || e.f != f || e.m != src.mass || e.device != dev || e.prec != lay.prec || e.D != lay.D ||
+            e.layers != lay.layers || e.pad != lay.pad || e.ra != fp.rows_alloc)
+            continue;
+        bool same = true;
+        for (int i = 0; i < kMaxDim; ++i) same &= e.n[i] == (i < lay.D ? lay.n[i] : 0);
+        if (same) {
+            *out = e.maps;
+            return true;
+        }
+    }
+    FzCacheEntry& e = g_fz_cache[g_fz_next];
+    g_fz_next = (g_fz_next + 1) % 8;
+    memset(&e.maps, 0, sizeof(e.maps));
+    if (!build_fused_maps(lay, src, fp, &e.maps)) {
+        e.valid = false;
+        return false;
+    }
+    e.valid = true;
+    e.f = f;
+    e.m = src.mass;
+    e.device = dev;
+    e.prec = lay.prec;
+    e.D = lay.D;
+    for (int i = 0; i < kMaxDim; ++i) e.n[i] = (i < lay.D) ? lay.n[i] : 0;
+    e.layers = lay.layers;
+    e.pad = lay.pad;
+    e.ra = fp.rows_alloc;
+    *out = e.maps;
+    return true;
+}
+
+template <int KK, int PREC>
+static cudaError_t launch_fused_k(const Layout& lay, const Sweep& s0, const Sweep& s1, const Arrays& src,
+                                  const Arrays& dst, const FusedPlan& fp, cudaStream_t s)
+{
+    FusedMaps maps;
+    if (!cached_fused_maps(lay, src, fp, &maps)) return cudaErrorInvalidValue;
+    int sms = 0, optin = 0;
+    tma_device_info(&sms, &optin);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(sweep_fused01_kernel<KK, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+        attr = true;
+    }
+    const int64_t ntiles = ((fp.nslab + fp.NS - 1) / fp.NS) * (lay.K / (KK * KK));
+    const int64_t grid = std::min<int64_t>(ntiles, sms);
+    if (grid < 1) return cudaSuccess;
+    const size_t smem = 256 + (size_t)fp.stages * fp.stage_bytes;
+    sweep_fused01_kernel<KK, PREC><<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, s0, s1, dst, fp, maps);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_fused01(const Layout& lay, const Sweep& s0, const Sweep& s1, const Arrays& src, const Arrays& dst,
+                           const FusedPlan& fp, cudaStream_t s)
+{
+    if (lay.prec == SLDG_FP64) {
+        switch (lay.k) {
+            case 1: return launch_fused_k<1, SLDG_FP64>(lay, s0, s1, src, dst, fp, s);
+            case 2: return launch_fused_k<2, SLDG_FP64>(lay, s0, s1, src, dst, fp, s);
+            case 3: return launch_fused_k<3, SLDG_FP64>(lay, s0, s1, src, dst, fp, s);
+        }
+    } else {
+        switch (lay.k) {
+            case 1: return launch_fused_k<1, SLDG_MIXED>(lay, s0, s1, src, dst, fp, s);
+            case 2: return launch_fused_k<2, SLDG_MIXED>(lay, s0, s1, src, dst, fp, s);
+            case 3: return launch_fused_k<3, SLDG_MIXED>(lay, s0, s1, src, dst, fp, s);
+        }
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace sldg

@@ -96,6 +96,7 @@ struct Grid {
     void* alloc[2] = {nullptr, nullptr};
     size_t alloc_bytes = 0;
     Weights w;
+    Weights w2;  // the second sweep's table of a fused pair (sldg_advect_pair)
     // the weight table holds the constant shift w_shift along an extent of w_n (no field):
     // a repeated constant-shift sweep reuses it instead of relaunching the build kernel
     bool w_const = false;
@@ -130,8 +131,8 @@ struct Grid {
     std::vector<double> ev_bytes;
     std::vector<int> ev_dim;
     std::vector<cudaEvent_t> ev_pool;
-    double prof_ms[kMaxDim] = {}, prof_bytes[kMaxDim] = {};
-    int64_t prof_launches[kMaxDim] = {};
+    double prof_ms[kMaxDim + 1] = {}, prof_bytes[kMaxDim + 1] = {};  // [kMaxDim]: fused pairs
+    int64_t prof_launches[kMaxDim + 1] = {};
     int64_t launches = 0;
 };
 
@@ -196,6 +197,21 @@ struct TmaPlan {
     int ctas = 1;   // CTAs per SM (shared-memory budget and register bound of the instance)
 };
 bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl);
+// fused dim-0 + dim-1 sweeps (sldg_fused.cu, NEXT-4 multi-sweep fusion)
+struct FusedPlan {
+    int NS = 0;          // slabs ("lanes") per tile = 256 / n0
+    int Tsub = 0;        // target rows per stage (the line's first stage loads one more row)
+    int rows_alloc = 0;  // Tsub + 1
+    int lane_bytes = 0;  // one lane's region of a stage
+    int stage_bytes = 0;
+    int stages = 0;
+    int64_t nslab = 0;   // local slabs (cells of dims >= 2)
+    int64_t M_mid = 0;   // prod_{2 <= d < D-1} n_d
+};
+bool fused_plan(const Layout& lay, const Sweep& s0, const Sweep& s1, FusedPlan* fp);
+cudaError_t launch_fused01(const Layout& lay, const Sweep& s0, const Sweep& s1, const Arrays& src, const Arrays& dst,
+                           const FusedPlan& fp, cudaStream_t s);
+void fused_cache_forget(const void* base, size_t bytes);
 const char* sweep_kernel_name(const Layout& lay, const Sweep& sw);
 // 1D sweeps, any precision layout (sldg_line.cu)
 cudaError_t launch_line(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst, cudaStream_t s,

@@ -23,7 +23,8 @@ STATUS_NAMES = {0: "OK", 1: "EINVAL", 2: "ENOMEM", 3: "ECUDA", 4: "ENCCL", 5: "E
 # every symbol include/sldg.h declares
 EXPORTS = [
     "sldg_create", "sldg_create_ex", "sldg_destroy", "sldg_set_coeffs", "sldg_get_coeffs", "sldg_advect",
-    "sldg_advect_device", "sldg_advect_device_bounded", "sldg_timeline", "sldg_mass", "sldg_shard_info", "sldg_sync", "sldg_set_stream",
+    "sldg_advect_device", "sldg_advect_device_bounded", "sldg_advect_pair", "sldg_advect_pair_device",
+    "sldg_timeline", "sldg_mass", "sldg_shard_info", "sldg_sync", "sldg_set_stream",
     "sldg_get_stream", "sldg_memory_bytes", "sldg_last_error", "sldg_fill_random",
     "sldg_fill_separable", "sldg_profile", "sldg_kernel_time", "sldg_launch_count",
     "sldg_nccl_unique_id", "sldg_halo_widths", "sldg_halo_plan", "sldg_layer_owner",
@@ -84,6 +85,8 @@ def lib():
                                        ctypes.c_double],
         "sldg_timeline": [vp, dp, ctypes.POINTER(ctypes.c_int), ctypes.c_int, ctypes.POINTER(ctypes.c_int),
                           ctypes.c_int],
+        "sldg_advect_pair": [vp, ctypes.c_double, dp, u32, ctypes.c_double, dp, u32],
+        "sldg_advect_pair_device": [vp, ctypes.c_double, vp, u32, ctypes.c_double, vp, u32],
         "sldg_mass": [vp, dp],
         "sldg_shard_info": [vp, i64p, i64p],
         "sldg_sync": [vp],
@@ -282,6 +285,31 @@ class Grid:
         its halo from the bound (no host synchronisation; graph-capturable)."""
         _check(lib().sldg_advect_device_bounded(self.h, int(dim), float(shift), ctypes.c_void_p(d_field_ptr),
                                                 ctypes.c_uint32(field_mask), float(nu_min), float(nu_max)))
+
+    def advect_pair(self, shift0: float = 0.0, field0=None, mask0: int = 0, shift1: float = 0.0, field1=None,
+                    mask1: int = 0):
+        """advect(0, shift0, field0, mask0) then advect(1, shift1, field1, mask1), in one pass over
+        HBM when the fields allow (sldg_advect_pair)."""
+        def arr(f, mask):
+            if f is None:
+                return None
+            f = np.ascontiguousarray(f, dtype=np.float64)
+            want = 1
+            for e in range(self.D):
+                if int(mask) >> e & 1:
+                    want *= self.cells[e]
+            if f.size != want:
+                raise SldgError(SLDG_EINVAL, f"shift field has {f.size} entries, field_mask {mask:#x} needs {want}")
+            return f
+        a0, a1 = arr(field0, mask0), arr(field1, mask1)
+        _check(lib().sldg_advect_pair(self.h, float(shift0), None if a0 is None else _dp(a0), ctypes.c_uint32(mask0),
+                                      float(shift1), None if a1 is None else _dp(a1), ctypes.c_uint32(mask1)))
+
+    def advect_pair_device(self, d_field0_ptr: int, mask0: int, d_field1_ptr: int, mask1: int,
+                           shift0: float = 0.0, shift1: float = 0.0):
+        _check(lib().sldg_advect_pair_device(self.h, float(shift0), ctypes.c_void_p(d_field0_ptr or None),
+                                             ctypes.c_uint32(mask0), float(shift1),
+                                             ctypes.c_void_p(d_field1_ptr or None), ctypes.c_uint32(mask1)))
 
     def timeline(self, reset: bool = True):
         """[(kind, t0_ms, t1_ms)] of the profiled sweeps (kind = dim) and halo exchanges (-1)."""

@@ -1,0 +1,7 @@
+O=gpurun_out/r2l; mkdir -p $O
+B="--no-cpu-baseline --no-e2e --no-compare-fp64 --no-vlasov"
+timeout 900 python -m pytest tests/test_gpu_fused.py -q -x -p no:cacheprovider > $O/pytest_fused.log 2>&1; echo rc=$? >> $O/pytest_fused.log
+for st in 3 2 4; do
+  SLDG_FUSED_STAGES=$st timeout 300 python bench.py --config c5 $B --fuse-x > $O/c5_fused_s$st.json 2> $O/c5_fused_s$st.err
+done
+timeout 300 python bench.py --config c4 $B --fuse-x > $O/c4_fused.json 2> $O/c4_fused.err
