@@ -43,7 +43,7 @@ namespace sldg {
 // B-source of target k - 1); it is cut into runs at every RA rows and at the wrap n1 - 1 -> 0, so
 // no box wraps.  Every lane of a tile takes the same number of stages (empty runs pad the lanes
 // whose line has no wrap inside).
-constexpr int kFzMaxRows = 8;
+constexpr int kFzMaxRows = 12;
 struct FusedMaps {
     CUtensorMap fA[kFzMaxRows];   // {n0, h rows, 1, k^2 planes}: fp32 planes (mixed) or all slots (fp64)
     CUtensorMap fA1[kFzMaxRows];  // mixed mass group: {n0, h, 1, k^2 - 1} fp32 planes
@@ -70,10 +70,15 @@ __host__ __device__ __forceinline__ void fz_run(int n1, int RA, int R0, int st, 
 // field entry of a slab (dims >= 2; s = i_mid + M_mid * local layer)
 __device__ __forceinline__ int64_t fz_field(const Sweep& sw, const Layout& lay, int64_t s, int64_t M_mid)
 {
-    int64_t im = s % M_mid, l = s / M_mid, f = 0;
+    // 32-bit index math (the plan bounds M_mid and the slab count), rolled loop: runs once per tile
+    const uint32_t mm = (uint32_t)M_mid;
+    uint32_t l = (uint32_t)s / mm, im = (uint32_t)s - l * mm;
+    int64_t f = 0;
+#pragma unroll 1
     for (int e = 2; e < lay.D - 1; ++e) {
-        f += (im % lay.n[e]) * sw.fstride[e];
-        im /= lay.n[e];
+        const uint32_t ne = (uint32_t)lay.n[e], q = im / ne;
+        f += (int64_t)(im - q * ne) * sw.fstride[e];
+        im = q;
     }
     return f + (lay.first_layer + l) * sw.fstride[lay.D - 1];
 }
@@ -343,13 +348,15 @@ bool fused_plan(const Layout& lay, const Sweep& s0, const Sweep& s1, FusedPlan* 
     const int k = lay.k, K2 = k * k;
     const int64_t M_mid = lay.L / (n0 * n1);
     const int64_t layers_alloc = lay.layers + 2 * lay.pad;
-    if (lay.L > ((int64_t)1 << 31) || layers_alloc > 65535 || M_mid > 65535) return false;
+    if (lay.L > ((int64_t)1 << 31) || layers_alloc > 65535 || M_mid > 65535 ||
+        M_mid * lay.layers > ((int64_t)1 << 31))
+        return false;
     fp->NS = (int)(256 / n0);
     fp->M_mid = M_mid;
     fp->nslab = M_mid * lay.layers;
     const int cell = (lay.prec == SLDG_FP64) ? 8 * K2 : 8 + 4 * (K2 - 1);  // bytes per cell of a group (max)
-    const int64_t budget = std::min<int64_t>(optin, 200 * 1024) - 256;
-    int stages = 3;
+    const int64_t budget = (int64_t)optin - 1024;  // one CTA per SM: the whole opt-in carveout
+    int stages = 2;  // measured on C5: 2 stages of <= 12 rows beat 3 and 4 smaller ones
     if (const char* e = getenv("SLDG_FUSED_STAGES")) stages = std::max(2, std::min(8, atoi(e)));
     int64_t ra = budget / stages / (256LL * cell);
     if (const char* e = getenv("SLDG_FUSED_TSUB")) ra = std::min<int64_t>(ra, atoi(e) + 1);
