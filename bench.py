@@ -305,7 +305,7 @@ def main():
                     help="diagnostic: run the layer-dim sweep through the sharded halo path on one GPU")
     ap.add_argument("--nccl-self", action="store_true",
                     help="diagnostic (with --force-halo): the self halo through NCCL send/recv")
-    ap.add_argument("--fuse-x", action=argparse.BooleanOptionalAction, default=False,
+    ap.add_argument("--fuse-x", action=argparse.BooleanOptionalAction, default=True,
                     help="run the dim-0 and dim-1 sweeps as one fused pass (sldg_advect_pair_device, NEXT-4)")
     ap.add_argument("--timeline", action="store_true",
                     help="record the device timeline of one step (sweeps + halo exchanges) into the JSON")
@@ -407,6 +407,7 @@ def main():
         if fuse:
             per_dim = {d: v for d, v in per_dim.items() if v[1] > 0}
             per_dim[-2] = g.kernel_time(-2)
+        g_kernel_names = {d: (g.sweep_kernel(d) if d >= 0 else "sweep_fused01_kernel") for d in per_dim}
         g.graph_begin()
         step()
         graph = g.graph_end()
@@ -444,6 +445,7 @@ def main():
         if fuse:
             per_dim = {d: v for d, v in per_dim.items() if v[1] > 0}
             per_dim[-2] = g.kernel_time(-2)
+        g_kernel_names = {d: (g.sweep_kernel(d) if d >= 0 else "sweep_fused01_kernel") for d in per_dim}
     if graph is not None:
         graph.destroy()
     t = torch.tensor([ms], dtype=torch.float64, device="cuda")
@@ -492,16 +494,28 @@ def main():
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * world,
                "api": "sldg_advect (host pinned CFL fields, one per sweep) + sldg_mass (D2H) per step"}
 
+    launch_steps = 2 if use_graph else args.steps  # steps the per-kernel events cover
     if rank == 0:
         peak, peak_src = load_peak()
         step_ms = ms_max / args.steps
         dofs_per_step = len(sweeps) * cells * K
         alg_bytes_step = len(sweeps) * 2 * cells * bytes_per_cell(K, args.precision)
         value = dofs_per_step / (step_ms * 1e-3) / 1e9
-        # dominant kernel = the sweep dim with the largest total kernel time (rank-0 view)
-        dom = max(per_dim, key=lambda d: per_dim[d][0])
-        d_ms, d_n, d_bytes = per_dim[dom]
+        # per kernel function (a template instance may serve several sweep dims): launches, time,
+        # algorithmic bytes; the dominant kernel is the one with the largest total time (rank 0)
+        kname = {d: (g_kernel_names[d]) for d in per_dim}
+        kernels = {}
+        for d, (ms_d, n_d, b_d) in per_dim.items():
+            e = kernels.setdefault(kname[d], {"ms": 0.0, "launches": 0, "bytes": 0.0, "dims": []})
+            e["ms"] += ms_d
+            e["launches"] += n_d
+            e["bytes"] += b_d
+            e["dims"].append(d if d >= 0 else "0+1")
+        dom_name = max(kernels, key=lambda kn: kernels[kn]["ms"])
+        dk = kernels[dom_name]
+        d_ms, d_n, d_bytes = dk["ms"], dk["launches"], dk["bytes"]
         achieved = (d_bytes / d_n) / (d_ms / d_n * 1e-3) / 1e9 if d_n else None
+        dom = max((d for d in per_dim if kname[d] == dom_name), key=lambda d: per_dim[d][0])
         traffic, traffic_all = None, None
         try:
             with open(os.path.join(ROOT, "profiles", "ncu_dram.json")) as f:
@@ -528,15 +542,25 @@ def main():
                          "traffic_source": "profiles/ncu_dram.json: dram__bytes_read.sum + dram__bytes_write.sum "
                                            "per launch of each sweep dim, ncu launch list of this config",
                          "algorithmic_bytes_per_sweep": 2 * cells * bytes_per_cell(K, args.precision),
-                         "kernel": (f"{g.sweep_kernel(dom)} (sweep along dim {dom})" if dom >= 0 else
-                                    "sweep_fused01_kernel (dims 0 + 1 in one pass: bytes of ONE read + write)"),
+                         "kernel": f"{dom_name} (sweeps along dims {dk['dims']})",
+                         "share_of_kernel_time": d_ms / max(1e-12, sum(e["ms"] for e in kernels.values())),
                          "peak_source": peak_src,
                          "frac_of_spec_8000": (achieved / 8000.0) if achieved else None,
                          "bytes_per_launch": d_bytes / d_n if d_n else None,
                          "launch_timing": ("CUDA events around each sweep launch in 2 eager steps before the "
                                            "graph-replayed timed region") if use_graph else
                                           "CUDA events around each sweep launch inside the timed region",
-                         "avg_launch_ms": d_ms / d_n if d_n else None},
+                         "avg_launch_ms": d_ms / d_n if d_n else None,
+                         "kernels": {kn: {"dims": e["dims"], "launches_per_step": e["launches"] / max(1, launch_steps),
+                                          "ms_per_launch": e["ms"] / max(1, e["launches"]),
+                                          "achieved_gbs": e["bytes"] / (e["ms"] * 1e-3) / 1e9 if e["ms"] else None,
+                                          "frac": (e["bytes"] / (e["ms"] * 1e-3) / 1e9 / peak) if e["ms"] else None,
+                                          "share": e["ms"] / max(1e-12, sum(x["ms"] for x in kernels.values()))}
+                                     for kn, e in kernels.items()},
+                         "bytes_note": ("algorithmic bytes = one read + one write of every stored coefficient per "
+                                        "launch (SURVEY 8(d)); the fused x1+x2 launch does two sweeps with ONE read + "
+                                        "write, so its per-sweep-equivalent rate is twice its achieved GB/s") if fuse else
+                                       "algorithmic bytes = one read + one write of every stored coefficient per sweep"},
             "fused_x": fuse,
             "sweeps": {(str(d) if d >= 0 else "fused01"): {"ms_per_launch": per_dim[d][0] / max(1, per_dim[d][1]),
                                 "gbs": (per_dim[d][2] / (per_dim[d][0] * 1e-3) / 1e9) if per_dim[d][0] else None}
@@ -650,7 +674,7 @@ def compare_precisions(args, dims, kinds, k):
     if int(np.prod(sdims)) * 8 * k ** len(dims) * 2 > 120e9:
         sdims[-1] = 32
     lo, hi = domain(kinds)
-    res = {"slab_dims": sdims}
+    res = {"slab_dims": sdims, "fused_x": bool(args.fuse_x)}
     for prec in ["mixed", "fp64"]:
         g = Grid(sdims, k, lo=lo, hi=hi, precision=prec)
         g.fill_separable(sldg_inputs.landau_terms(sdims, k, kinds, lo, hi, eps=args.eps))
@@ -658,16 +682,24 @@ def compare_precisions(args, dims, kinds, k):
         dfs = [torch.tensor(f, dtype=torch.float64, device="cuda") for _, f, _ in sweeps]
         torch.cuda.synchronize()
         stream = torch.cuda.ExternalStream(g.stream())
-        for _ in range(2):
-            for (d, _, m), tf in zip(sweeps, dfs):
+        fuse = args.fuse_x and len(sweeps) >= 2 and sweeps[0][0] == 0 and sweeps[1][0] == 1
+
+        def step():  # the same split step as the timed one (fused x pair when enabled)
+            first = 0
+            if fuse:
+                g.advect_pair_device(dfs[0].data_ptr(), sweeps[0][2], dfs[1].data_ptr(), sweeps[1][2])
+                first = 2
+            for (d, _, m), tf in list(zip(sweeps, dfs))[first:]:
                 g.advect_device(d, tf.data_ptr(), m)
+
+        for _ in range(2):
+            step()
         g.sync()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             e0.record(stream)
         for _ in range(3):
-            for (d, _, m), tf in zip(sweeps, dfs):
-                g.advect_device(d, tf.data_ptr(), m)
+            step()
         with torch.cuda.stream(stream):
             e1.record(stream)
         g.sync()

@@ -443,6 +443,18 @@ sldg_status vp_x_sweeps(sldg_vp vp, double tau)
             VCU(cudaGetLastError());
             g->launches += 1;
             st = sldg_advect_vnodes_device(g, c, dv, vp->d_nux[c]);
+        } else if (c == 0 && vp->dx >= 2) {
+            // x1 and x2 together: their CFL numbers depend only on v1 / v2, so the pair runs in one
+            // pass over HBM (sldg_advect_pair_device, bit-identical to the two sweeps)
+            const int dv1 = vp->dx + 1;
+            const int64_t nv1 = g->lay.n[dv1];
+            vp_x_field_kernel<<<nblk(nv), 256, 0, g->stream>>>(nv, g->lo[dv], g->h[dv], tau, g->h[0], vp->d_nux[0]);
+            VCU(cudaGetLastError());
+            vp_x_field_kernel<<<nblk(nv1), 256, 0, g->stream>>>(nv1, g->lo[dv1], g->h[dv1], tau, g->h[1], vp->d_nux[1]);
+            VCU(cudaGetLastError());
+            g->launches += 2;
+            st = sldg_advect_pair_device(g, 0.0, vp->d_nux[0], 1u << dv, 0.0, vp->d_nux[1], 1u << dv1);
+            ++c;  // x2 done
         } else {
             vp_x_field_kernel<<<nblk(nv), 256, 0, g->stream>>>(nv, g->lo[dv], g->h[dv], tau, g->h[c], vp->d_nux[c]);
             VCU(cudaGetLastError());

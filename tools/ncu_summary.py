@@ -66,9 +66,14 @@ def launches(path, out, dram_json=None, key=None):
         # (after bench.py's default 3 warm-up steps), not the e2e / precision-comparison runs
         ndim = int(key.split("_D")[-1]) if "_D" in key else 4
         base = key.split("_D")[0]
-        first = sweeps[3 * ndim:4 * ndim]
-        for dim, d in enumerate(first):
-            db[f"{base}_dim{dim}"] = d.get("read", 0) + d.get("write", 0)
+        # a step is ndim sweep launches in dim order, or with the fused x pair (bench default)
+        # sweep_fused01_kernel then dims 2 .. ndim-1
+        fused = any("fused01" in d["name"] for d in sweeps)
+        per_step = ndim - 1 if fused else ndim
+        names = (["fused01"] + [f"dim{e}" for e in range(2, ndim)]) if fused else [f"dim{e}" for e in range(ndim)]
+        first = sweeps[3 * per_step:4 * per_step]
+        for nm, d in zip(names, first):
+            db[f"{base}_{nm}"] = d.get("read", 0) + d.get("write", 0)
         json.dump(db, open(dram_json, "w"), indent=1, sort_keys=True)
     print(out)
 
