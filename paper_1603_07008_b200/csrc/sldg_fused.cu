@@ -470,11 +470,7 @@ static cudaError_t launch_fused_k(const Layout& lay, const Sweep& s0, const Swee
     if (!cached_fused_maps(lay, src, fp, &maps)) return cudaErrorInvalidValue;
     int sms = 0, optin = 0;
     tma_device_info(&sms, &optin);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(sweep_fused01_kernel<KK, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
-        attr = true;
-    }
+    ensure_max_smem((const void*)sweep_fused01_kernel<KK, PREC>);
     const int64_t ntiles = ((fp.nslab + fp.NS - 1) / fp.NS) * (lay.K / (KK * KK));
     const int64_t grid = std::min<int64_t>(ntiles, sms);
     if (grid < 1) return cudaSuccess;

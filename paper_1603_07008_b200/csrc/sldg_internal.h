@@ -197,6 +197,9 @@ struct TmaPlan {
     int ctas = 1;   // CTAs per SM (shared-memory budget and register bound of the instance)
 };
 bool tma_plan(const Layout& lay, const Sweep& sw, TmaPlan* pl);
+// cudaFuncAttributeMaxDynamicSharedMemorySize = the opt-in maximum for `func` on the CURRENT device
+// (set once per (device, function); the attribute is per device context)
+void ensure_max_smem(const void* func);
 // fused dim-0 + dim-1 sweeps (sldg_fused.cu, NEXT-4 multi-sweep fusion)
 struct FusedPlan {
     int NS = 0;          // slabs ("lanes") per tile = 256 / n0

@@ -306,11 +306,7 @@ static cudaError_t launch_line_tma(const Layout& lay, const Sweep& sw, const Arr
                                    const LinePlan& lp, cudaStream_t s)
 {
     auto kern = line_tma_kernel<KK, NDJ>;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_optin);
-        attr = true;
-    }
+    ensure_max_smem((const void*)kern);  // full opt-in carveout (per device)
     const size_t smem = 256 + (size_t)lp.stages * lp.stage_bytes;
     const int64_t ntiles = (lay.n[0] + lp.Wt - 1) / lp.Wt;
     const int64_t grid = std::min<int64_t>(ntiles, g_sms);

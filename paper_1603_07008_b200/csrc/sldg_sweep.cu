@@ -450,11 +450,8 @@ cudaError_t launch_sweep(const Layout& lay, const Sweep& sw, const Arrays& src, 
     *n_launched = (layer_end > layer_begin) ? 1 : 0;
     // TMA-staged kernels when the shapes allow (sldg_sweep_tma.cu); SLDG_SWEEP=reg forces the
     // register kernels below (A/B comparisons and tests of both paths).
-    static int mode = -1;
-    if (mode < 0) {
-        const char* e = getenv("SLDG_SWEEP");
-        mode = (e && e[0] == 'r') ? 0 : 1;
-    }
+    const char* env = getenv("SLDG_SWEEP");  // read per call: the switch may change within a process
+    const int mode = (env && env[0] == 'r') ? 0 : 1;
     // 1D grids (the paper's workload, any precision layout): the line kernels (sldg_line.cu)
     if (lay.D == 1 && (mode == 1 || lay.prec == SLDG_GENERAL)) return launch_line(lay, sw, src, dst, s, nullptr);
     TmaPlan pl;

@@ -1065,6 +1065,21 @@ static bool make_tmap(CUtensorMap* tm, bool f64, void* base, const int64_t* dims
     return r == CUDA_SUCCESS;
 }
 
+void ensure_max_smem(const void* func)
+{
+    static std::mutex mu;
+    static std::vector<std::pair<int, const void*>> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& d : done)
+        if (d.first == dev && d.second == func) return;
+    int optin = 0;
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, optin);
+    done.push_back({dev, func});
+}
+
 bool make_tmap5(CUtensorMap* tm, bool f64, void* base, const int64_t* dims, const int64_t* strides, const int* box)
 {
     return make_tmap(tm, f64, base, dims, strides, box);
@@ -1391,11 +1406,7 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
     if (sw.dim == 0) {
         ntiles = ((lay.L / lay.n[0] + pl.R - 1) / pl.R) * (le - lb);
         auto kern = (pl.ctas == 2) ? sweep_d0_tma<KK, PREC, 2> : sweep_d0_tma<KK, PREC, 1>;
-        static bool attr_set[3] = {false, false, false};  // once per instantiation: full opt-in carveout
-        if (!attr_set[pl.ctas]) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
-            attr_set[pl.ctas] = true;
-        }
+        ensure_max_smem((const void*)kern);  // full opt-in carveout
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, g_num_sms - sw.sm_reserve) * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
@@ -1409,11 +1420,7 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         ntiles = ((nline + pl.T - 1) / pl.T) * (M_lo / pl.W) * M_hi * (outer ? 1 : (le - lb));
         auto kern = (pl.ctas == 2) ? (pl.pspan ? sweep_strided_tma<KK, PREC, 2, true> : sweep_strided_tma<KK, PREC, 2, false>)
                                    : (pl.pspan ? sweep_strided_tma<KK, PREC, 1, true> : sweep_strided_tma<KK, PREC, 1, false>);
-        static bool attr_set[3][2] = {};  // once per instantiation: full opt-in carveout
-        if (!attr_set[pl.ctas][pl.pspan]) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, g_smem_optin);
-            attr_set[pl.ctas][pl.pspan] = true;
-        }
+        ensure_max_smem((const void*)kern);  // full opt-in carveout
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, g_num_sms - sw.sm_reserve) * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
