@@ -57,6 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     hdr_t = max(os.path.getmtime(p) for p in headers())
     flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{inc}",
              f"-I{os.path.join(ROOT, 'include')}"] + (["-Xptxas", "-v"] if verbose else [])
+    flags += os.environ.get("SLDG_NVCC_EXTRA", "").split()  # A/B variant builds (e.g. -DFZ_ROW_UNROLL=2)
 
     def compile_one(src):
         obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")

@@ -44,6 +44,10 @@ namespace sldg {
 // no box wraps.  Every lane of a tile takes the same number of stages (empty runs pad the lanes
 // whose line has no wrap inside).
 constexpr int kFzMaxRows = 12;
+#ifndef FZ_ROW_UNROLL
+#define FZ_ROW_UNROLL 1
+#endif
+constexpr int kFzRowUnroll = FZ_ROW_UNROLL;
 struct FusedMaps {
     CUtensorMap fA[kFzMaxRows];   // {n0, h rows, 1, k^2 planes}: fp32 planes (mixed) or all slots (fp64)
     CUtensorMap fA1[kFzMaxRows];  // mixed mass group: {n0, h, 1, k^2 - 1} fp32 planes
@@ -103,7 +107,7 @@ __device__ __forceinline__ void fz_rows(FzLine<KK>& ln, const unsigned char* lba
     constexpr int E = (PREC == SLDG_FP64) ? 8 : 4;
     const int pb = h * n0 * E;                                          // bytes per (non-mass) slot
     const int mshift = (MASSG && PREC == SLDG_MIXED) ? h * n0 * 4 : 0;  // the fp64 mass slot is wider
-#pragma unroll 1
+#pragma unroll(kFzRowUnroll)
     for (int r = 0; r < h; ++r) {
         const int ea = r * n0 + ln.ca, eb = r * n0 + ln.cb;
         double x1[K2];

@@ -25,11 +25,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
 #include <mutex>
+#include <vector>
 
 #include "sldg_internal.h"
 #include "sldg_ptx.cuh"
@@ -41,6 +43,21 @@ struct TmapSet {
     CUtensorMap f[kTmaHeights];  // fp32 planes (mixed) or all slots (fp64)
     CUtensorMap m[kTmaHeights];  // fp64 mass slot (mixed)
 };
+
+#ifdef SLDG_STAMPS
+// diagnostic builds (-DSLDG_STAMPS): per-CTA %globaltimer stamps of the strided kernel, printed by
+// the launcher (start, first stage ready, consumers done, producer done)
+__device__ unsigned long long g_stamp[4 * 1024];
+__device__ __forceinline__ unsigned long long gtimer()
+{
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define SLDG_STAMP(i) g_stamp[4 * blockIdx.x + (i)] = gtimer()
+#else
+#define SLDG_STAMP(i) ((void)0)
+#endif
 
 template <int PREC>
 __device__ __forceinline__ int64_t toff_m(const Layout& L, int64_t layerp, int64_t inner)
@@ -278,6 +295,10 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
         }
     }
     __syncthreads();
+    if (threadIdx.x == 0) SLDG_STAMP(0);
+#ifdef SLDG_STAMPS
+    bool first_full = true;
+#endif
 
     const int D = lay.D, d = sw.dim;
     const bool outer = (d == D - 1);
@@ -653,6 +674,10 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
                     __syncwarp();
                 } else {
                     mbar_wait(&full[s], ph);
+#ifdef SLDG_STAMPS
+                    if (first_full && threadIdx.x == 0) SLDG_STAMP(1);
+                    first_full = false;
+#endif
                     if (lo_t < hi_t) {
                         const unsigned char* sb[KK];
                         char* op[KK];
@@ -689,6 +714,8 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
             }
         }
     }
+    if (threadIdx.x == 0) SLDG_STAMP(2);
+    if (producer && lane == 0) SLDG_STAMP(3);
 }
 
 // ============================================================================================
@@ -1424,6 +1451,32 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, g_num_sms - sw.sm_reserve) * per_sm);
         if (grid < 1) return cudaSuccess;
         kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
+#ifdef SLDG_STAMPS
+        {
+            std::vector<unsigned long long> h((size_t)4 * grid);
+            cudaStreamSynchronize(s);
+            cudaMemcpyFromSymbol(h.data(), g_stamp, h.size() * 8);
+            unsigned long long t0 = ~0ull;
+            for (int64_t b = 0; b < grid; ++b) t0 = std::min(t0, h[4 * b]);
+            std::vector<double> st, ff, cd, pd;
+            for (int64_t b = 0; b < grid; ++b) {
+                st.push_back((h[4 * b] - t0) * 1e-3);
+                ff.push_back((h[4 * b + 1] - h[4 * b]) * 1e-3);
+                cd.push_back((h[4 * b + 2] - t0) * 1e-3);
+                pd.push_back((h[4 * b + 3] - t0) * 1e-3);
+            }
+            auto q = [](std::vector<double> v, double f) {
+                std::sort(v.begin(), v.end());
+                return v[(size_t)(f * (v.size() - 1) + 0.5)];
+            };
+            fprintf(stderr,
+                    "SLDG_STAMP strided dim=%d W=%d T=%d Tsub=%d stages=%d pspan=%d grid=%lld ntiles=%lld: start max %.1f "
+                    "us; first stage after start p50 %.1f max %.1f; consumers done p0 %.1f p50 %.1f max %.1f; "
+                    "producer done max %.1f us\n",
+                    sw.dim, pl.W, pl.T, pl.Tsub, pl.stages, pl.pspan, (long long)grid, (long long)ntiles, q(st, 1.0),
+                    q(ff, 0.5), q(ff, 1.0), q(cd, 0.0), q(cd, 0.5), q(cd, 1.0), q(pd, 1.0));
+        }
+#endif
     } else {
         return cudaErrorInvalidValue;  // strided k > 4: the plan never selects it
     }

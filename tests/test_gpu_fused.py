@@ -131,3 +131,35 @@ def test_pair_c5_full_size_sampled(eps):
     b = np.concatenate([g.get_coeffs(int(x), 1) for x in cells])
     g.destroy()
     assert a.tobytes() == b.tobytes()
+
+
+def test_pair_device_fields_and_graph_capture():
+    """sldg_advect_pair_device (fields in HBM) equals the host-field pair, and a captured step
+    of two pairs replays bit-identically."""
+    dims, k = [128, 16, 6, 5], 3
+    rng = np.random.default_rng(9)
+    f0 = rng.uniform(-2.5, 2.5, dims[2])
+    f1 = rng.uniform(-1.5, 3.5, dims[3])
+    d0 = torch.tensor(f0, dtype=torch.float64, device="cuda")
+    d1 = torch.tensor(f1, dtype=torch.float64, device="cuda")
+    c = sldg_inputs.random_coeffs(dims, k, 21)
+    g = _Grid(dims, k)
+    g.set_coeffs(c)
+    g.advect_pair(0.0, f0, 0b100, 0.0, f1, 0b1000)
+    host = g.get_coeffs()
+    g.set_coeffs(c)
+    g.advect_pair_device(d0.data_ptr(), 0b100, d1.data_ptr(), 0b1000)
+    assert g.get_coeffs().tobytes() == host.tobytes()
+    g.set_coeffs(c)
+    g.graph_begin()
+    g.advect_pair_device(d0.data_ptr(), 0b100, d1.data_ptr(), 0b1000)
+    g.advect_pair_device(d0.data_ptr(), 0b100, d1.data_ptr(), 0b1000)
+    gr = g.graph_end()
+    gr.launch()
+    replay = g.get_coeffs()
+    g.set_coeffs(c)
+    g.advect_pair_device(d0.data_ptr(), 0b100, d1.data_ptr(), 0b1000)
+    g.advect_pair_device(d0.data_ptr(), 0b100, d1.data_ptr(), 0b1000)
+    assert g.get_coeffs().tobytes() == replay.tobytes()
+    gr.destroy()
+    g.destroy()
