@@ -214,6 +214,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         }
     }
     __syncthreads();
+    pdl_wait();  // the weights and the source array come from the preceding kernels
 
     const int G = lay.K / K2;
     const int64_t M_mid = fp.M_mid;
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     if (producer) {
         if (lane == 0) {
             for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+                if (tile + gridDim.x >= ntiles) pdl_trigger();  // this CTA's last tile
                 const int gq = (int)(tile % G);
                 const int64_t sg = tile / G;
                 const bool massg = (PREC == SLDG_MIXED) && gq == 0;
@@ -276,6 +278,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     const int tid = threadIdx.x;
     const int b = tid / n0, c = tid % n0;
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (tile + gridDim.x >= ntiles) pdl_trigger();  // this CTA's last tile
         const int gq = (int)(tile % G);
         const int64_t sg = tile / G;
         const bool massg = (PREC == SLDG_MIXED) && gq == 0;
@@ -479,8 +482,8 @@ static cudaError_t launch_fused_k(const Layout& lay, const Sweep& s0, const Swee
     const int64_t grid = std::min<int64_t>(ntiles, sms);
     if (grid < 1) return cudaSuccess;
     const size_t smem = 256 + (size_t)fp.stages * fp.stage_bytes;
-    sweep_fused01_kernel<KK, PREC><<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, s0, s1, dst, fp, maps);
-    return cudaGetLastError();
+    return launch_pdl(sweep_fused01_kernel<KK, PREC>, dim3((unsigned)grid), dim3(kTmaThreads), smem, s, lay, s0, s1,
+                      dst, fp, maps);
 }
 
 cudaError_t launch_fused01(const Layout& lay, const Sweep& s0, const Sweep& s1, const Arrays& src, const Arrays& dst,

@@ -16,6 +16,7 @@
 
 #include "sldg_basis.cuh"
 #include "sldg_internal.h"
+#include "sldg_ptx.cuh"
 
 namespace sldg {
 
@@ -46,6 +47,10 @@ __global__ void __launch_bounds__(32) build_weights_kernel(int64_t nd, const dou
                                      double* __restrict__ ab, double* __restrict__ rec, int* __restrict__ err,
                                      const GaussTab gt, int64_t ilo, int64_t ihi)
 {
+    // PDL: let the sweep that reads these weights launch now; wait for the previous sweep (which
+    // reads the table this kernel overwrites) before writing
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (e >= n_entries) return;
     const double nu = field ? field[e] : shift;
@@ -150,9 +155,10 @@ cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field,
     int threads = 32;
     int64_t blocks = (n_entries + threads - 1) / threads;
     const GaussTab& gt = gauss_table(lay.k);
+    cudaError_t lerr = cudaSuccess;
 #define SLDG_W(KK)                                                                                           \
-    build_weights_kernel<KK><<<(unsigned)blocks, threads, 0, s>>>(nd, d_field, shift, n_entries, w.shift, w.smod, \
-                                                                  w.copy, w.ab, w.rec, d_err, gt, ilo, ihi)
+    lerr = launch_pdl(build_weights_kernel<KK>, dim3((unsigned)blocks), dim3(threads), 0, s, nd, d_field, shift, n_entries, \
+               w.shift, w.smod, w.copy, w.ab, w.rec, d_err, gt, ilo, ihi)
     switch (lay.k) {
         case 1: SLDG_W(1); break;
         case 2: SLDG_W(2); break;
@@ -165,6 +171,7 @@ cudaError_t launch_weights(const Layout& lay, int64_t nd, const double* d_field,
         default: return cudaErrorInvalidValue;
     }
 #undef SLDG_W
+    if (lerr != cudaSuccess) return lerr;
     return cudaGetLastError();
 }
 

@@ -4,6 +4,9 @@
 #include <cuda.h>  // CUtensorMap (types only)
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
+
+#include <utility>
 
 namespace sldg {
 
@@ -26,17 +29,32 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar)
 {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifndef SLDG_MBAR_HINT_NS
+#define SLDG_MBAR_HINT_NS 1000000u  // suspend-time hint of mbarrier waits (ns); 0: plain try_wait spin
+#endif
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity)
 {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(1000000u)  // suspend-time hint (ns): sleep until the phase completes
-        : "memory");
+    if (SLDG_MBAR_HINT_NS == 0) {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+            "@!p bra WAIT_%=;\n"
+            "}\n" ::"r"(smem_u32(bar)),
+            "r"(parity)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n"
+            ".reg .pred p;\n"
+            "WAIT_%=:\n"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+            "@!p bra WAIT_%=;\n"
+            "}\n" ::"r"(smem_u32(bar)),
+            "r"(parity), "r"(SLDG_MBAR_HINT_NS)  // suspend-time hint (ns): sleep until the phase completes
+            : "memory");
+    }
 }
 // 1D bulk copy global -> shared (fallback for rows that wrap around a periodic line)
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t pol)
@@ -72,6 +90,34 @@ __device__ __forceinline__ uint64_t policy_evict_first()
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
+}
+
+// Programmatic dependent launch (PDL): a kernel launched with the programmatic-serialization
+// attribute may start while its predecessor in the stream finishes; pdl_wait() blocks until the
+// predecessor grid has completed and its writes are visible (no-op without PDL), pdl_trigger()
+// lets the successor launch once every CTA of this grid has triggered or exited.  The sweep kernels
+// trigger at the start of their LAST tile (all their CTAs are resident by then, so a successor's
+// waiting CTAs can never hold an SM one of ours still needs); the weight build at its start.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// launch with the PDL attribute (SLDG_PDL=0 disables it: plain stream order)
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                                     Args&&... args)
+{
+    static const bool on = !(getenv("SLDG_PDL") && atoi(getenv("SLDG_PDL")) == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = on ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // 5D tile tensor map (sldg_sweep_tma.cu): dims / strides in elements (strides[0] = 1 implied),

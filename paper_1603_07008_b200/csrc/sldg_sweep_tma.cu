@@ -47,14 +47,14 @@ struct TmapSet {
 #ifdef SLDG_STAMPS
 // diagnostic builds (-DSLDG_STAMPS): per-CTA %globaltimer stamps of the strided kernel, printed by
 // the launcher (start, first stage ready, consumers done, producer done)
-__device__ unsigned long long g_stamp[4 * 1024];
+__device__ unsigned long long g_stamp[8 * 1024];
 __device__ __forceinline__ unsigned long long gtimer()
 {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-#define SLDG_STAMP(i) g_stamp[4 * blockIdx.x + (i)] = gtimer()
+#define SLDG_STAMP(i) g_stamp[8 * blockIdx.x + (i)] = gtimer()
 #else
 #define SLDG_STAMP(i) ((void)0)
 #endif
@@ -295,6 +295,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
         }
     }
     __syncthreads();
+    pdl_wait();  // the weights and the source array come from the preceding kernels
     if (threadIdx.x == 0) SLDG_STAMP(0);
 #ifdef SLDG_STAMPS
     bool first_full = true;
@@ -423,6 +424,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
     uint32_t it = 0;  // stage-use counter, identical in every warp
     uint32_t tcount = 0;  // tiles of this CTA so far, identical in every warp
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++tcount) {
+        if (tile + gridDim.x >= ntiles) pdl_trigger();  // this CTA's last tile
         int64_t cb, hi, layer, t0;
         decode(tile, cb, hi, layer, t0);
         const int nt = (int)((nline - t0) < T ? (nline - t0) : T);
@@ -633,6 +635,9 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
                 unsigned char* st = stage0 + (size_t)s * pl.stage_bytes;
                 if (producer) {
                     if (lane == 0) {
+#ifdef SLDG_STAMPS
+                        if (it == 1) SLDG_STAMP(4);
+#endif
                         mbar_wait(&empty[s], ph ^ 1);
                         uint32_t bytes = 0;
 #pragma unroll
@@ -670,9 +675,15 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
                             }
                             soff += Rmax * W * es;
                         }
+#ifdef SLDG_STAMPS
+                        if (it == 1) SLDG_STAMP(5);
+#endif
                     }
                     __syncwarp();
                 } else {
+#ifdef SLDG_STAMPS
+                    if (first_full && threadIdx.x == 0) SLDG_STAMP(6);
+#endif
                     mbar_wait(&full[s], ph);
 #ifdef SLDG_STAMPS
                     if (first_full && threadIdx.x == 0) SLDG_STAMP(1);
@@ -905,6 +916,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
         }
     }
     __syncthreads();
+    pdl_wait();  // the weights and the source array come from the preceding kernels
 
     const int D = lay.D;
     const int n0 = (int)lay.n[0];
@@ -939,6 +951,7 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
     int my_cp = 0;
     double wr[SMW ? 1 : 2 * KK * KK];
     for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (tile + gridDim.x >= ntiles) pdl_trigger();  // this CTA's last tile
         const int64_t blk = tile % nblk;
         const int64_t layer = lb + tile / nblk;
         const int64_t layerp = lay.pad + layer;
@@ -1436,7 +1449,9 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         ensure_max_smem((const void*)kern);  // full opt-in carveout
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, g_num_sms - sw.sm_reserve) * per_sm);
         if (grid < 1) return cudaSuccess;
-        kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
+        cudaError_t le0 = launch_pdl(kern, dim3((unsigned)grid), dim3(kTmaThreads), smem, s, lay, sw, src, dst, lb, le, pl,
+                                     tmaps);
+        if (le0 != cudaSuccess) return le0;
     } else if constexpr (KK <= 6) {
         const bool outer = (sw.dim == lay.D - 1);
         const int64_t nline = outer ? (le - lb) : sw.nd;
@@ -1450,20 +1465,25 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
         ensure_max_smem((const void*)kern);  // full opt-in carveout
         int64_t grid = std::min<int64_t>(ntiles, (int64_t)std::max(1, g_num_sms - sw.sm_reserve) * per_sm);
         if (grid < 1) return cudaSuccess;
-        kern<<<(unsigned)grid, kTmaThreads, smem, s>>>(lay, sw, src, dst, lb, le, pl, tmaps);
+        cudaError_t le1 = launch_pdl(kern, dim3((unsigned)grid), dim3(kTmaThreads), smem, s, lay, sw, src, dst, lb, le, pl,
+                                     tmaps);
+        if (le1 != cudaSuccess) return le1;
 #ifdef SLDG_STAMPS
         {
-            std::vector<unsigned long long> h((size_t)4 * grid);
+            std::vector<unsigned long long> h((size_t)8 * grid);
             cudaStreamSynchronize(s);
             cudaMemcpyFromSymbol(h.data(), g_stamp, h.size() * 8);
             unsigned long long t0 = ~0ull;
-            for (int64_t b = 0; b < grid; ++b) t0 = std::min(t0, h[4 * b]);
-            std::vector<double> st, ff, cd, pd;
+            for (int64_t b = 0; b < grid; ++b) t0 = std::min(t0, h[8 * b]);
+            std::vector<double> st, ff, cd, pd, pe, pi, cw;
             for (int64_t b = 0; b < grid; ++b) {
-                st.push_back((h[4 * b] - t0) * 1e-3);
-                ff.push_back((h[4 * b + 1] - h[4 * b]) * 1e-3);
-                cd.push_back((h[4 * b + 2] - t0) * 1e-3);
-                pd.push_back((h[4 * b + 3] - t0) * 1e-3);
+                st.push_back((h[8 * b] - t0) * 1e-3);
+                ff.push_back((h[8 * b + 1] - h[8 * b]) * 1e-3);
+                cd.push_back((h[8 * b + 2] - t0) * 1e-3);
+                pd.push_back((h[8 * b + 3] - t0) * 1e-3);
+                pe.push_back((h[8 * b + 4] - h[8 * b]) * 1e-3);
+                pi.push_back((h[8 * b + 5] - h[8 * b]) * 1e-3);
+                cw.push_back((h[8 * b + 6] - h[8 * b]) * 1e-3);
             }
             auto q = [](std::vector<double> v, double f) {
                 std::sort(v.begin(), v.end());
@@ -1475,6 +1495,9 @@ static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays
                     "producer done max %.1f us\n",
                     sw.dim, pl.W, pl.T, pl.Tsub, pl.stages, pl.pspan, (long long)grid, (long long)ntiles, q(st, 1.0),
                     q(ff, 0.5), q(ff, 1.0), q(cd, 0.0), q(cd, 0.5), q(cd, 1.0), q(pd, 1.0));
+            fprintf(stderr, "SLDG_STAMP   first stage: producer at its empty wait p50 %.1f, TMAs issued p50 %.1f max %.1f, "
+                            "consumers at their full wait p50 %.1f us after start\n",
+                    q(pe, 0.5), q(pi, 0.5), q(pi, 1.0), q(cw, 0.5));
         }
 #endif
     } else {

@@ -1,0 +1,6 @@
+O=gpurun_out/r2s; mkdir -p $O
+B="--no-cpu-baseline --no-e2e --no-compare-fp64 --no-vlasov"
+for c in c2 c3 c5; do
+  st=2; [ $c = c5 ] && st=1
+  (cd _ab_stamp && timeout 300 python bench.py --config $c --steps $st --warmup 3 $B --no-graph > $GRAFT_REPO_ROOT/$O/$c.json 2> $GRAFT_REPO_ROOT/$O/$c.err)
+done
