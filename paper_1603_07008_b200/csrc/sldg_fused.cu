@@ -87,6 +87,25 @@ __device__ __forceinline__ int64_t fz_field(const Sweep& sw, const Layout& lay, 
     return f + (lay.first_layer + l) * sw.fstride[lay.D - 1];
 }
 
+// The rounded intermediate of the mixed layout, widened on the integer ALU instead of F2F (the XU
+// pipe bounds this kernel): the fp32 bits placed in the fp64 fields give the value times 2^-896,
+// exactly, for every finite value (zero and subnormals included); the x2 weights are pre-scaled
+// by 2^896 (exact), so each FMA sees the product of the unscaled contraction.  The mass slot of
+// the mass group stays unscaled fp64 and meets its weights unscaled at the point of use.
+__device__ __forceinline__ double fz_f32_scaled(float f)
+{
+    const uint32_t u = __float_as_uint(f);
+    const uint32_t hi = (uint32_t)((int32_t)u >> 3) & 0x8FFFFFFFu;
+    return __hiloint2double((int)hi, (int)(u << 29));
+}
+constexpr double kFzScale = 0x1p896;
+__device__ __forceinline__ double fz_unscale(double w)  // w 2^-896, not hoisted out of the row loop
+{
+    double r;
+    asm volatile("mul.rn.f64 %0, %1, 0d07F0000000000000;" : "=d"(r) : "d"(w));
+    return r;
+}
+
 // one consumer thread's line state: weights of both sweeps, source columns, the carried A-part
 template <int KK>
 struct FzLine {
@@ -144,7 +163,8 @@ __device__ __forceinline__ void fz_rows(FzLine<KK>& ln, const unsigned char* lba
                     }
                     v = oa + ob;
                 }
-                x1[j] = dbl ? v : (double)__double2float_rn(v);  // the stored intermediate
+                // the stored intermediate (mixed fp32 slots: widened scaled, see fz_f32_scaled)
+                x1[j] = dbl ? v : fz_f32_scaled(__double2float_rn(v));
             }
         }
         const int k = k0 + r;
@@ -157,11 +177,17 @@ __device__ __forceinline__ void fz_rows(FzLine<KK>& ln, const unsigned char* lba
                     const int j = m0 + KK * m1o;
                     double o;
                     if (CPY && ln.cp1) {
-                        o = x1[j];  // alpha = 0: exact copy of the B-source (R4)
+                        // alpha = 0: exact copy of the B-source (R4); a scaled fp32 value is unscaled exactly
+                        const bool dj = PREC == SLDG_FP64 || (MASSG && j == 0);
+                        o = dj ? x1[j] : x1[j] * kFzScale;
                     } else {
                         o = ln.sA[j];  // the carried A-part, then the B terms (sweep_strided_tma's order)
 #pragma unroll
-                        for (int m1 = 0; m1 < KK; ++m1) o = fma(ln.B2[m1o * KK + m1], x1[m0 + KK * m1], o);
+                        for (int m1 = 0; m1 < KK; ++m1) {
+                            const bool mass_in = PREC == SLDG_MIXED && MASSG && m0 == 0 && m1 == 0;
+                            const double w = mass_in ? fz_unscale(ln.B2[m1o * KK + m1]) : ln.B2[m1o * KK + m1];
+                            o = fma(w, x1[m0 + KK * m1], o);
+                        }
                     }
                     if (PREC == SLDG_FP64)
                         __stcs(ln.o64 + off + (int64_t)j * L, o);
@@ -178,7 +204,11 @@ __device__ __forceinline__ void fz_rows(FzLine<KK>& ln, const unsigned char* lba
             for (int m1o = 0; m1o < KK; ++m1o) {
                 double a = 0.0;
 #pragma unroll
-                for (int m1 = 0; m1 < KK; ++m1) a = fma(ln.A2[m1o * KK + m1], x1[m0 + KK * m1], a);
+                for (int m1 = 0; m1 < KK; ++m1) {
+                    const bool mass_in = PREC == SLDG_MIXED && MASSG && m0 == 0 && m1 == 0;
+                    const double w = mass_in ? fz_unscale(ln.A2[m1o * KK + m1]) : ln.A2[m1o * KK + m1];
+                    a = fma(w, x1[m0 + KK * m1], a);
+                }
                 ln.sA[m0 + KK * m1o] = a;
             }
     }
@@ -293,6 +323,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 ln.B1[i] = __ldg(&s0.ab[f0 * 2 * K2 + K2 + i]);
                 ln.A2[i] = __ldg(&s1.ab[f1 * 2 * K2 + i]);
                 ln.B2[i] = __ldg(&s1.ab[f1 * 2 * K2 + K2 + i]);
+                if (PREC == SLDG_MIXED) {  // they meet intermediates scaled by 2^-896 (fz_f32_scaled)
+                    ln.A2[i] *= kFzScale;
+                    ln.B2[i] *= kFzScale;
+                }
             }
             const int i1s = (int)__ldg(&s0.smod[f0]);
             const int i2s = (int)__ldg(&s1.smod[f1]);
