@@ -141,9 +141,9 @@ __device__ __forceinline__ void fz_rows(FzLine<KK>& ln, const unsigned char* lba
                 if (dbl) {
                     va[m0] = ((const double*)p)[ea];
                     vb[m0] = ((const double*)p)[eb];
-                } else {
-                    va[m0] = (double)((const float*)p)[ea];
-                    vb[m0] = (double)((const float*)p)[eb];
+                } else {  // scaled by 2^-896 (fz_f32_scaled); A1 / B1 carry 2^896
+                    va[m0] = fz_f32_scaled(((const float*)p)[ea]);
+                    vb[m0] = fz_f32_scaled(((const float*)p)[eb]);
                 }
             }
 #pragma unroll
@@ -152,14 +152,17 @@ __device__ __forceinline__ void fz_rows(FzLine<KK>& ln, const unsigned char* lba
                 const bool dbl = PREC == SLDG_FP64 || (MASSG && j == 0);
                 double v;
                 if (CPY && ln.cp0) {
-                    v = vb[m0];  // alpha = 0: exact copy (R4)
+                    v = dbl ? vb[m0] : vb[m0] * kFzScale;  // alpha = 0: exact copy (R4), unscaled exactly
                 } else {
                     // A- and B-parts as two chains, then one add (sweep_d0_tma's order)
                     double oa = 0.0, ob = 0.0;
 #pragma unroll
                     for (int l = 0; l < KK; ++l) {
-                        oa = fma(ln.A1[m0 * KK + l], va[l], oa);
-                        ob = fma(ln.B1[m0 * KK + l], vb[l], ob);
+                        const bool mass_in = PREC == SLDG_MIXED && MASSG && m1 == 0 && l == 0;
+                        const double wa = mass_in ? fz_unscale(ln.A1[m0 * KK + l]) : ln.A1[m0 * KK + l];
+                        const double wb = mass_in ? fz_unscale(ln.B1[m0 * KK + l]) : ln.B1[m0 * KK + l];
+                        oa = fma(wa, va[l], oa);
+                        ob = fma(wb, vb[l], ob);
                     }
                     v = oa + ob;
                 }
@@ -321,6 +324,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             for (int i = 0; i < K2; ++i) {
                 ln.A1[i] = __ldg(&s0.ab[f0 * 2 * K2 + i]);
                 ln.B1[i] = __ldg(&s0.ab[f0 * 2 * K2 + K2 + i]);
+                if (PREC == SLDG_MIXED) {  // they meet inputs scaled by 2^-896 (fz_f32_scaled)
+                    ln.A1[i] *= kFzScale;
+                    ln.B1[i] *= kFzScale;
+                }
                 ln.A2[i] = __ldg(&s1.ab[f1 * 2 * K2 + i]);
                 ln.B2[i] = __ldg(&s1.ab[f1 * 2 * K2 + K2 + i]);
                 if (PREC == SLDG_MIXED) {  // they meet intermediates scaled by 2^-896 (fz_f32_scaled)
