@@ -296,6 +296,18 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_strided_tma(Layout la
     }
     __syncthreads();
     pdl_wait();  // the weights and the source array come from the preceding kernels
+#ifdef SLDG_WARM_TMA
+    // diagnostic: touch every tensor map with an L2 prefetch of one box before the span work
+    if (threadIdx.x == kTmaConsumerWarps * 32) {
+        for (int h = 0; h < kTmaHeights; ++h) {
+            asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %1, %1, %1, %2}];" ::"l"(
+                             (uint64_t)&tmaps.f[h]), "r"(0), "r"((int)lay.pad) : "memory");
+            if (PREC == SLDG_MIXED)
+                asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.tile [%0, {%1, %1, %1, %1, %2}];" ::"l"(
+                                 (uint64_t)&tmaps.m[h]), "r"(0), "r"((int)lay.pad) : "memory");
+        }
+    }
+#endif
     if (threadIdx.x == 0) SLDG_STAMP(0);
 #ifdef SLDG_STAMPS
     bool first_full = true;
