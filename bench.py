@@ -393,7 +393,9 @@ def main():
     # graph, else from the timed steps themselves
     # graphs only where the host's per-call cost shows (steps of < 1e9 DoF: C2-C4); C5's timed
     # region stays eager so the per-kernel events are taken inside it
-    use_graph = args.graph and len(sweeps) % 2 == 0 and len(sweeps) * cells * K / world < 1e9
+    # (one GPU only: sharded grids capture too -- tested with the NCCL self-exchange -- but real
+    # multi-rank NCCL inside a capture has not run on hardware here)
+    use_graph = args.graph and world == 1 and len(sweeps) % 2 == 0 and len(sweeps) * cells * K < 1e9
     graph = None
     if use_graph:
         g.kernel_time(reset=True)
