@@ -216,8 +216,8 @@ sldg_status sldg_kernel_time(sldg_grid g, int dim, double* ms, int64_t* launches
  * (kinds[i] = its dim; -2 for a fused sweep pair) and every halo exchange on the comm stream
  * (kinds[i] = -1), in the order
  * they were enqueued: 2 doubles per entry in t_ms.  Shows whether the interior sweep of a
- * sharded sweep overlaps its halo exchange.  *n_out = number of recorded entries (up to
- * max_entries are written); reset != 0 clears them.  Blocks. */
+ * sharded sweep overlaps its halo exchange.  *n_out = number of recorded entries (the first 4096
+ * after a reset are kept; up to max_entries are written); reset != 0 clears them.  Blocks. */
 sldg_status sldg_timeline(sldg_grid g, double* t_ms, int* kinds, int max_entries, int* n_out, int reset);
 /* Number of kernels this handle has launched (all kinds). */
 int64_t sldg_launch_count(sldg_grid g);

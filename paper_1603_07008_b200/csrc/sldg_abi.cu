@@ -193,6 +193,8 @@ cudaEvent_t pool_event(sldg_grid g)
 }
 
 // Launch one sweep kernel over local layers [lb, le) with optional profiling events.
+constexpr size_t kTimelineMax = 4096;  // profiled intervals kept for sldg_timeline
+
 sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arrays& dst, int64_t lb, int64_t le,
                       const Layout* lay = nullptr)
 {
@@ -217,8 +219,13 @@ sldg_status run_sweep(sldg_grid g, const Sweep& sw, const Arrays& src, const Arr
         g->ev_pairs.push_back({e0, e1});
         g->ev_bytes.push_back(2.0 * (double)bytes_per_cell(LY) * (double)((le - lb) * LY.L));
         g->ev_dim.push_back(sw.dim);
-        g->tl_ev.push_back({t0, t1});
-        g->tl_kind.push_back(sw.dim);
+        if (g->tl_ev.size() < kTimelineMax) {  // bounded: a long profiled run keeps its first entries
+            g->tl_ev.push_back({t0, t1});
+            g->tl_kind.push_back(sw.dim);
+        } else {
+            g->ev_pool.push_back(t0);
+            g->ev_pool.push_back(t1);
+        }
     }
     return SLDG_OK;
 }
@@ -636,8 +643,13 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
         if (st != SLDG_OK) return st;
         if (g->profile) {
             CU(cudaEventRecord(h1, g->comm_stream));
-            g->tl_ev.push_back({h0, h1});
-            g->tl_kind.push_back(-1);
+            if (g->tl_ev.size() < kTimelineMax) {
+                g->tl_ev.push_back({h0, h1});
+                g->tl_kind.push_back(-1);
+            } else {
+                g->ev_pool.push_back(h0);
+                g->ev_pool.push_back(h1);
+            }
         }
         CU(cudaEventRecord(g->ev_halo, g->comm_stream));
         // interior layers need no halo: overlap them with the exchange, leaving comm_sms SMs to
@@ -770,8 +782,13 @@ sldg_status advect_pair_impl(sldg_grid g, double shift0, const double* f0, uint3
         g->ev_pairs.push_back({e0, e1});
         g->ev_bytes.push_back(2.0 * (double)bytes_per_cell(L) * (double)L.cells);  // ONE read + write: two sweeps
         g->ev_dim.push_back(kMaxDim);
-        g->tl_ev.push_back({t0, t1});
-        g->tl_kind.push_back(-2);
+        if (g->tl_ev.size() < kTimelineMax) {
+            g->tl_ev.push_back({t0, t1});
+            g->tl_kind.push_back(-2);
+        } else {
+            g->ev_pool.push_back(t0);
+            g->ev_pool.push_back(t1);
+        }
     }
     g->cur = 1 - g->cur;
     return SLDG_OK;
