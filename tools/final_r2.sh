@@ -1,6 +1,6 @@
 # Round-2 final evidence: GPU tests, smoke, the default bench line (with its reference arm), bench
 # lines of the other configs / precisions, and the unfused C5 split step.  -> gpurun_out/final/
-O=gpurun_out/final; mkdir -p $O
+O=${O:-gpurun_out/final}; mkdir -p $O
 nvidia-smi -q -d CLOCK,POWER > $O/smi.txt 2>&1
 timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo rc=$? >> $O/pytest_gpu.log
 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
