@@ -305,6 +305,9 @@ def main():
                     help="diagnostic: run the layer-dim sweep through the sharded halo path on one GPU")
     ap.add_argument("--nccl-self", action="store_true",
                     help="diagnostic (with --force-halo): the self halo through NCCL send/recv")
+    ap.add_argument("--peer-halo", action="store_true",
+                    help="pad layers mapped onto the ring neighbours' edge layers (SLDG_DIST_PEER_HALO); with one "
+                         "GPU implies --force-halo (the rank's own edges)")
     ap.add_argument("--fuse-x", action=argparse.BooleanOptionalAction, default=True,
                     help="run the dim-0 and dim-1 sweeps as one fused pass (sldg_advect_pair_device, NEXT-4)")
     ap.add_argument("--timeline", action="store_true",
@@ -325,6 +328,8 @@ def main():
     cells = int(np.prod(dims))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if args.peer_halo and world == 1:
+        args.force_halo = True
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     sweep_dims = list(range(D)) if args.sweeps is None else [int(x) for x in args.sweeps.split(",")]
     cfg_json = {"workload": f"{args.config}: {desc}", "dims": dims, "k": k, "coeffs_per_cell": K,
@@ -355,7 +360,7 @@ def main():
 
     lo, hi = domain(kinds)
     g = Grid(dims, k, lo=lo, hi=hi, precision=args.precision, rank=rank, world=world, unique_id=uid,
-             max_halo=2, force_halo=args.force_halo, nccl_self=args.nccl_self)
+             max_halo=2, force_halo=args.force_halo, nccl_self=args.nccl_self, peer_halo=args.peer_halo)
     terms = sldg_inputs.landau_terms(dims, k, kinds, lo, hi, eps=args.eps)
     g.fill_separable(terms)
     sweeps = [s for s in sldg_inputs.vlasov_fields(dims, kinds, lo, hi, eps=args.eps) if s[0] in sweep_dims]
@@ -462,7 +467,7 @@ def main():
         g.profile(True)
         g.timeline(reset=True)
         step()
-        timeline = [{"kind": "halo" if kd < 0 else f"sweep dim {kd}", "t0_ms": a, "t1_ms": b}
+        timeline = [{"kind": "halo" if kd == -1 else "fused dims 0+1" if kd == -2 else f"sweep dim {kd}", "t0_ms": a, "t1_ms": b}
                     for kd, a, b in g.timeline(reset=True)]
         g.profile(False)
         g.kernel_time(reset=True)
@@ -581,7 +586,10 @@ def main():
         if timeline is not None:
             out["timeline"] = timeline
         if args.force_halo:
-            out["config"]["diagnostic"] = "forced halo path on one GPU" + (" (NCCL self)" if args.nccl_self else "")
+            out["config"]["diagnostic"] = "forced halo path on one GPU" + (" (NCCL self)" if args.nccl_self else "") \
+                + (" (peer-mapped pads)" if args.peer_halo else "")
+        if args.peer_halo:
+            out["config"]["halo"] = "peer-mapped"
     vp_res = None
     if args.vlasov and world == 1 and args.sweeps is None:
         vp_res = time_vlasov(g, stream, dims, kinds, k)

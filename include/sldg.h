@@ -103,6 +103,17 @@ typedef struct {
  * device copies -- the multi-GPU NCCL code paths (message pointers, counts, pairing order)
  * exercised on one GPU. */
 #define SLDG_DIST_NCCL_SELF 4
+/* Peer-mapped halos: the pad layers of both coefficient arrays are CUDA
+ * virtual-memory mappings of the ring neighbours' edge layers (left pad = the left neighbour's
+ * last `max_halo` layers, right pad = the right neighbour's first ones; with world == 1 and
+ * SLDG_DIST_FORCE_HALO, this rank's own).  A sweep along the sharded dim whose halo fits the
+ * pads is then ONE launch over all local layers whose boundary tiles read the neighbours' HBM
+ * directly (NVLink for another GPU): no exchange step.  world > 1: an NCCL fence with both
+ * neighbours before and after such a sweep (device-side, capturable); the chunks are shared
+ * between processes as POSIX file descriptors (pidfd_getfd).  Creation is collective and fails
+ * with ENOTSUP unless sldg_peer_halo_check accepts the layout at the device's allocation
+ * granularity. */
+#define SLDG_DIST_PEER_HALO 8
 
 /* Create a grid (zero-filled).  k in 1..SLDG_MAX_K coefficients per dim (the paper's order
  * o = p+1).  dist may be NULL (single GPU).  The device is the caller's current
@@ -276,6 +287,14 @@ sldg_status sldg_layer_owner(int64_t n, int world, int64_t layer, int* owner, in
  * for p = 0..world-1 (out holds 8 * world int64).  The forward and inverse messages of
  * sldg_advect follow exactly this plan (inverse = the same pairs reversed). */
 sldg_status sldg_transpose_plan(int64_t n_outer, int64_t n_slab, int world, int rank, int64_t* out);
+/* Host-only check of SLDG_DIST_PEER_HALO for a grid (`prec` SLDG_MIXED or SLDG_FP64, k, the
+ * global extents), `world` ranks, `pad` halo layers per side and allocation granularity `gran`
+ * bytes (the device's minimum; 2 MiB on B200): every rank must hold >= 2 pad layers, and pad
+ * and every rank's layer count times the per-layer bytes of each precision section (fp64
+ * planes, fp32 planes) must be multiples of gran.  SLDG_OK, else ENOTSUP with the reason in
+ * sldg_last_error(); EINVAL for bad arguments. */
+sldg_status sldg_peer_halo_check(const sldg_grid_desc* grid, int k, sldg_precision prec, int world, int pad,
+                                 int64_t gran);
 /* Number of sweeps of this handle that took the transpose path. */
 sldg_status sldg_transpose_count(sldg_grid g, int64_t* n);
 

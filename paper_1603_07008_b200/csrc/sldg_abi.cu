@@ -623,6 +623,17 @@ sldg_status advect_impl(sldg_grid g, int dim, double shift, const double* field,
     } else {
         int64_t left = std::max<int64_t>(0, imax + 1), right = std::max<int64_t>(0, -imin);
         const int P = g->world;
+        if (g->peer_halo && !g->force_transpose && left <= L.pad && right <= L.pad) {
+            // the pads ARE the neighbours' edge layers: one launch over all local layers, its pad
+            // boxes read the neighbours' memory directly; fences order it against their sweeps
+            sw.wrap = 0;
+            CU(peer_fence(g));
+            st = run_sweep(g, sw, src, dst, 0, L.layers);
+            if (st != SLDG_OK) return st;
+            CU(peer_fence(g));
+            g->cur = 1 - g->cur;
+            return SLDG_OK;
+        }
         if (g->force_transpose || left > L.pad || right > L.pad ||
             (P > 1 && (left + right) * P > 2 * L.layers * (P - 1))) {
             st = transpose_sweep(g, sw, dfield, shift, n_entries, src, dst);
@@ -922,6 +933,31 @@ sldg_status sldg_advect_vnodes_device(sldg_grid g, int dim, int vdim, const doub
     return advect_vnodes_impl(g, dim, vdim, d_nodal_nu, true);
 }
 
+sldg_status sldg_peer_halo_check(const sldg_grid_desc* grid, int k, sldg_precision prec, int world, int pad,
+                                 int64_t gran)
+{
+    if (!grid || grid->ndim < 1 || grid->ndim > SLDG_MAX_DIM || k < 1 || k > SLDG_MAX_K || world < 1 || pad < 0 ||
+        gran < 1 || (prec != SLDG_MIXED && prec != SLDG_FP64))
+        return fail(SLDG_EINVAL, "bad arguments");
+    Layout L{};
+    L.D = grid->ndim;
+    L.k = k;
+    int64_t K = 1, cells_per_layer = 1;
+    for (int d = 0; d < L.D; ++d) {
+        if (grid->cells[d] < 1) return fail(SLDG_EINVAL, "cells must be >= 1");
+        K *= k;
+        L.n[d] = grid->cells[d];
+        if (d < L.D - 1) cells_per_layer *= grid->cells[d];
+    }
+    if (L.D >= 2 && grid->cells[L.D - 1] < world) return fail(SLDG_EINVAL, "sharded extent smaller than world");
+    L.K = (int)K;
+    L.nd = (prec == SLDG_MIXED && K > 1) ? 1 : (int)K;
+    L.L = cells_per_layer;
+    L.pad = pad;
+    std::string why = peer_halo_check(L, world, (size_t)gran);
+    return why.empty() ? SLDG_OK : fail(SLDG_ENOTSUP, why);
+}
+
 sldg_status sldg_transpose_count(sldg_grid g, int64_t* n)
 {
     if (!g || !n) return fail(SLDG_EINVAL, "null argument");
@@ -1019,6 +1055,7 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
     g->halo_mode = (world > 1) || (dist && (dist->flags & (SLDG_DIST_FORCE_HALO | SLDG_DIST_FORCE_TRANSPOSE)) && D >= 2);
     g->force_transpose = dist && (dist->flags & SLDG_DIST_FORCE_TRANSPOSE) && D >= 2;
     g->nccl_self = dist && (dist->flags & SLDG_DIST_NCCL_SELF) && world == 1;
+    g->peer_halo = g->halo_mode && (dist->flags & SLDG_DIST_PEER_HALO);
     L.pad = g->halo_mode ? ((dist->max_halo > 0) ? dist->max_halo : 2) : 0;
     L.cells = L.layers * L.L;
     g->rank = rank;
@@ -1040,16 +1077,6 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
     {  // the minimum weight table (constant shifts): such sweeps never allocate, also inside a capture
         sldg_status ws = ensure_weights(g, 1);
         if (ws != SLDG_OK) return bail(ws);
-    }
-    g->alloc_bytes = array_alloc_bytes(L);
-    for (int b = 0; b < 2; ++b) {
-        cudaError_t e = cudaMalloc(&g->alloc[b], g->alloc_bytes);
-        if (e != cudaSuccess)
-            return bail(fail(SLDG_ENOMEM, "device allocation of " + std::to_string(g->alloc_bytes) +
-                                              " bytes failed: " + cudaGetErrorString(e)));
-        if (cudaMemsetAsync(g->alloc[b], 0, g->alloc_bytes, g->stream) != cudaSuccess)
-            return bail(fail(SLDG_ECUDA, "memset failed"));
-        g->buf[b] = arrays_of(L, g->alloc[b]);
     }
     if (cudaMalloc(&g->d_partials, kMassBlocks * sizeof(double)) != cudaSuccess ||
         cudaMalloc(&g->d_scalar, 64 * sizeof(double)) != cudaSuccess ||
@@ -1081,6 +1108,21 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
             g->own_comm = true;
         }
     }
+    g->alloc_bytes = array_alloc_bytes(L);
+    if (g->peer_halo) {  // pads mapped onto the neighbours' edge layers (sldg_peer.cu); collective
+        std::string why = peer_alloc(g);
+        if (!why.empty()) return bail(fail(SLDG_ENOTSUP, "SLDG_DIST_PEER_HALO: " + why));
+        for (int b = 0; b < 2; ++b) g->buf[b] = arrays_of(L, g->alloc[b]);
+    }
+    for (int b = 0; b < 2 && !g->peer_halo; ++b) {
+        cudaError_t e = cudaMalloc(&g->alloc[b], g->alloc_bytes);
+        if (e != cudaSuccess)
+            return bail(fail(SLDG_ENOMEM, "device allocation of " + std::to_string(g->alloc_bytes) +
+                                              " bytes failed: " + cudaGetErrorString(e)));
+        if (cudaMemsetAsync(g->alloc[b], 0, g->alloc_bytes, g->stream) != cudaSuccess)
+            return bail(fail(SLDG_ECUDA, "memset failed"));
+        g->buf[b] = arrays_of(L, g->alloc[b]);
+    }
     if (cudaStreamSynchronize(g->stream) != cudaSuccess) return bail(fail(SLDG_ECUDA, "sync failed"));
     *out = g;
     return SLDG_OK;
@@ -1095,8 +1137,9 @@ sldg_status sldg_destroy(sldg_grid g)
     for (int b = 0; b < 2; ++b) {
         tmap_cache_forget(g->alloc[b], g->alloc_bytes);
         fused_cache_forget(g->alloc[b], g->alloc_bytes);
-        cudaFree(g->alloc[b]);
+        if (!g->peer) cudaFree(g->alloc[b]);
     }
+    peer_free(g);
     tmap_cache_forget(g->t_alloc, g->t_bytes);
     cudaFree(g->w2.shift);
     cudaFree(g->w2.smod);

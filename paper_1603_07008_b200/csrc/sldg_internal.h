@@ -245,6 +245,9 @@ struct sldg_grid_s : public sldg::Grid {
     // launch, for the overlap timeline (sldg_timeline)
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> tl_ev;
     std::vector<int> tl_kind;      // sweep dim, or -1 for a halo exchange
+    // SLDG_DIST_PEER_HALO: the pad layers are mappings of the neighbours' edge layers (sldg_peer.cu)
+    bool peer_halo = false;
+    struct sldg_peer_s* peer = nullptr;
     double* d_vnrec = nullptr;     // Gauss-node sweep: per-v-cell operator records
     int64_t vnrec_cap = 0;
     // graph capture (sldg_graph_begin/end)
@@ -252,3 +255,14 @@ struct sldg_grid_s : public sldg::Grid {
     int cap_cur = 0;
     int64_t cap_launches = 0;
 };
+
+// peer-mapped halo layers (sldg_peer.cu)
+namespace sldg {
+// "" if the layout can back its pads with the neighbours' edge chunks at allocation granularity
+// `gran` on every rank of `world`, else the reason
+std::string peer_halo_check(const Layout& L, int world, size_t gran);
+size_t peer_granularity(int device);  // 0 if the virtual-memory API is unavailable
+std::string peer_alloc(sldg_grid g);  // sets g->alloc[0..1] and g->peer; "" or the reason
+void peer_free(sldg_grid g);
+cudaError_t peer_fence(sldg_grid g);  // world > 1: NCCL fence with both ring neighbours
+}  // namespace sldg

@@ -1,0 +1,328 @@
+// sldg_peer.cu -- peer-mapped halo layers (SLDG_DIST_PEER_HALO; DESIGN.md §7 "Peer-mapped halos").
+//
+// A sweep along the sharded layer dim reads source rows i - i* - 1 and i - i* (P:214-219), so
+// its first and last layers need up to `pad` layers owned by the ring neighbours.  The NCCL path
+// copies those layers into this rank's pad layers before the boundary layers are swept.  Here
+// the pad layers are not memory of their own: with the CUDA virtual-memory API each coefficient
+// array is one reserved address range in which
+//   the local layers are backed by this rank's physical allocations, split per section (the fp64
+//   planes, then the fp32 planes) into a low chunk (layers [0, pad)), a middle chunk and a high
+//   chunk (layers [layers - pad, layers)), and
+//   the left pad is a second mapping of the LEFT neighbour's high chunk, the right pad one of the
+//   RIGHT neighbour's low chunk (the same buffer of the ping-pong pair, the same section).
+// The sweep kernels are unchanged: their TMA boxes that fall in a pad read the neighbour's HBM
+// directly (over NVLink for another GPU), so the transfer happens inside the sweep, tile by tile,
+// with no exchange step, no NCCL kernel and no SM reserve.  With world == 1 (forced halo) the
+// neighbour is this rank itself: the pads alias its own opposite boundary layers.
+//
+// Ordering across ranks (world > 1): a sharded sweep reads the neighbours' CURRENT source
+// buffer, so each rank's previous sweep must be complete before it starts, and the neighbours
+// must not overwrite that buffer (their next sweep writes it: ping-pong) before it ends.  Both
+// are one NCCL send/recv fence with the two ring neighbours on the grid's stream, before and
+// after the sweep (a fence completes only once the peer's stream has reached it).
+//
+// Physical chunks must be multiples of the allocation granularity at granularity-aligned
+// offsets: pad * u and layers * u are multiples of it for both sections' per-layer bytes u, on
+// every rank (peer_halo_check).  Cross-process mapping (world > 1) exports each chunk as a POSIX
+// file descriptor; the descriptors are fetched with pidfd_getfd(2) after an NCCL all-gather of
+// (pid, fd) -- this part needs two GPUs and is not exercised by the one-GPU tests.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <sys/prctl.h>
+#include <sys/syscall.h>
+#include <unistd.h>
+
+#include <string>
+#include <vector>
+
+#include "sldg_internal.h"
+
+namespace sldg {
+
+namespace {
+
+#define SLDG_DRV(name) decltype(&::name) name = nullptr
+struct Driver {
+    SLDG_DRV(cuMemGetAllocationGranularity);
+    SLDG_DRV(cuMemCreate);
+    SLDG_DRV(cuMemRelease);
+    SLDG_DRV(cuMemAddressReserve);
+    SLDG_DRV(cuMemAddressFree);
+    SLDG_DRV(cuMemMap);
+    SLDG_DRV(cuMemUnmap);
+    SLDG_DRV(cuMemSetAccess);
+    SLDG_DRV(cuMemExportToShareableHandle);
+    SLDG_DRV(cuMemImportFromShareableHandle);
+    bool ok = false;
+};
+#undef SLDG_DRV
+
+const Driver& drv()
+{
+    static Driver d = [] {
+        Driver r;
+        bool ok = true;
+        auto get = [&](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess ||
+                q != cudaDriverEntryPointSuccess || !*fn)
+                ok = false;
+        };
+        get("cuMemGetAllocationGranularity", (void**)&r.cuMemGetAllocationGranularity);
+        get("cuMemCreate", (void**)&r.cuMemCreate);
+        get("cuMemRelease", (void**)&r.cuMemRelease);
+        get("cuMemAddressReserve", (void**)&r.cuMemAddressReserve);
+        get("cuMemAddressFree", (void**)&r.cuMemAddressFree);
+        get("cuMemMap", (void**)&r.cuMemMap);
+        get("cuMemUnmap", (void**)&r.cuMemUnmap);
+        get("cuMemSetAccess", (void**)&r.cuMemSetAccess);
+        get("cuMemExportToShareableHandle", (void**)&r.cuMemExportToShareableHandle);
+        get("cuMemImportFromShareableHandle", (void**)&r.cuMemImportFromShareableHandle);
+        r.ok = ok;
+        return r;
+    }();
+    return d;
+}
+
+CUmemAllocationProp alloc_prop(int device, bool shareable)
+{
+    CUmemAllocationProp p = {};
+    p.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+    p.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    p.location.id = device;
+    p.requestedHandleTypes = shareable ? CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR : CU_MEM_HANDLE_TYPE_NONE;
+    return p;
+}
+
+// per-layer bytes of the two sections of one array (sldg_internal.h layout); u32 may be 0
+void section_units(const Layout& L, size_t* u64, size_t* u32)
+{
+    *u64 = (size_t)L.L * 8 * (size_t)L.nd;
+    *u32 = (size_t)L.L * 4 * (size_t)(L.K - L.nd);
+}
+
+}  // namespace
+
+std::string peer_halo_check(const Layout& L, int world, size_t gran)
+{
+    if (L.D < 2) return "peer-mapped halos need D >= 2 (a sharded layer dim)";
+    if (L.pad < 1) return "peer-mapped halos need pad >= 1";
+    size_t u[2];
+    section_units(L, &u[0], &u[1]);
+    const int64_t n = L.n[L.D - 1];
+    for (int r = 0; r < world; ++r) {
+        const int64_t layers = n / world + ((r < n % world) ? 1 : 0);
+        if (layers < 2 * L.pad)
+            return "rank " + std::to_string(r) + " holds " + std::to_string(layers) + " layers < 2 * pad = " +
+                   std::to_string(2 * L.pad) + " (its low and high chunks would overlap)";
+        for (int s = 0; s < 2; ++s) {
+            if (!u[s]) continue;
+            if (((size_t)L.pad * u[s]) % gran || ((size_t)layers * u[s]) % gran)
+                return std::string(s ? "fp32" : "fp64") + " section: pad * " + std::to_string(u[s]) + " B and " +
+                       std::to_string(layers) + " layers * " + std::to_string(u[s]) +
+                       " B must be multiples of the allocation granularity " + std::to_string(gran) + " B";
+        }
+    }
+    return "";
+}
+
+size_t peer_granularity(int device)
+{
+    const Driver& d = drv();
+    if (!d.ok) return 0;
+    CUmemAllocationProp p = alloc_prop(device, false);
+    size_t g = 0;
+    if (d.cuMemGetAllocationGranularity(&g, &p, CU_MEM_ALLOC_GRANULARITY_MINIMUM) != CUDA_SUCCESS) return 0;
+    return g;
+}
+
+}  // namespace sldg
+
+using namespace sldg;
+
+// Chunk bookkeeping of one grid (sldg_grid_s::peer)
+struct sldg_peer_s {
+    struct Map {
+        CUdeviceptr va;
+        size_t bytes;
+    };
+    CUdeviceptr base[2] = {0, 0};
+    size_t bytes = 0;
+    std::vector<CUmemGenericAllocationHandle> handles;  // created or imported here: released at free
+    std::vector<Map> maps;
+    // this rank's low / high chunk handles per (buffer, section): [b][s][0 = low, 1 = high]
+    CUmemGenericAllocationHandle edge[2][2][2] = {};
+    int* d_fence = nullptr;  // fence words (world > 1)
+};
+
+namespace sldg {
+
+void peer_free(sldg_grid g)
+{
+    sldg_peer_s* P = g->peer;
+    if (!P) return;
+    const Driver& d = drv();
+    for (const auto& m : P->maps) d.cuMemUnmap(m.va, m.bytes);
+    for (auto h : P->handles) d.cuMemRelease(h);
+    for (int b = 0; b < 2; ++b)
+        if (P->base[b]) d.cuMemAddressFree(P->base[b], P->bytes);
+    if (P->d_fence) cudaFree(P->d_fence);
+    delete P;
+    g->peer = nullptr;
+    g->alloc[0] = g->alloc[1] = nullptr;
+}
+
+// Reserve both arrays, back their local layers with this rank's chunks, map the neighbours'
+// edge chunks into the pads.  Returns "" or the reason (the caller destroys the grid).
+std::string peer_alloc(sldg_grid g)
+{
+    const Layout& L = g->lay;
+    const Driver& d = drv();
+    if (!d.ok) return "the CUDA virtual-memory driver entry points are unavailable";
+    const size_t gran = peer_granularity(g->device);
+    if (!gran) return "cuMemGetAllocationGranularity failed";
+    std::string why = peer_halo_check(L, g->world, gran);
+    if (!why.empty()) return why;
+    const bool shared = g->world > 1;
+    CUmemAllocationProp prop = alloc_prop(g->device, shared);
+    sldg_peer_s* P = new sldg_peer_s();
+    g->peer = P;
+    size_t u[2];
+    section_units(L, &u[0], &u[1]);
+    const size_t p = (size_t)L.pad, nl = (size_t)L.layers;
+    const size_t sec_bytes[2] = {(nl + 2 * p) * u[0], (nl + 2 * p) * u[1]};
+    P->bytes = sec_bytes[0] + sec_bytes[1];
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = g->device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    auto map = [&](CUdeviceptr va, size_t bytes, CUmemGenericAllocationHandle h) -> bool {
+        if (d.cuMemMap(va, bytes, 0, h, 0) != CUDA_SUCCESS) return false;
+        P->maps.push_back({va, bytes});
+        return d.cuMemSetAccess(va, bytes, &acc, 1) == CUDA_SUCCESS;
+    };
+    auto create = [&](size_t bytes, CUmemGenericAllocationHandle* h) -> bool {
+        if (d.cuMemCreate(h, bytes, &prop, 0) != CUDA_SUCCESS) return false;
+        P->handles.push_back(*h);
+        return true;
+    };
+    for (int b = 0; b < 2; ++b) {
+        if (d.cuMemAddressReserve(&P->base[b], P->bytes, gran, 0, 0) != CUDA_SUCCESS)
+            return "cuMemAddressReserve of " + std::to_string(P->bytes) + " bytes failed";
+        size_t off = 0;
+        for (int s = 0; s < 2; ++s) {
+            if (!u[s]) continue;
+            const CUdeviceptr sec = P->base[b] + off;
+            CUmemGenericAllocationHandle lo, mid, hi;
+            if (!create(p * u[s], &lo) || !map(sec + p * u[s], p * u[s], lo)) return "low chunk allocation failed";
+            if (nl > 2 * p && (!create((nl - 2 * p) * u[s], &mid) || !map(sec + 2 * p * u[s], (nl - 2 * p) * u[s], mid)))
+                return "middle chunk allocation failed";
+            if (!create(p * u[s], &hi) || !map(sec + nl * u[s], p * u[s], hi)) return "high chunk allocation failed";
+            P->edge[b][s][0] = lo;
+            P->edge[b][s][1] = hi;
+            if (cudaMemsetAsync((void*)(sec + p * u[s]), 0, nl * u[s], g->stream) != cudaSuccess)
+                return "memset failed";
+            off += sec_bytes[s];
+        }
+    }
+    if (cudaStreamSynchronize(g->stream) != cudaSuccess) return "memset failed";
+    // the neighbours' edge chunks: [b][s][0] = left neighbour's high, [1] = right neighbour's low
+    CUmemGenericAllocationHandle nb[2][2][2] = {};
+    if (!shared) {
+        for (int b = 0; b < 2; ++b)
+            for (int s = 0; s < 2; ++s) {
+                nb[b][s][0] = P->edge[b][s][1];
+                nb[b][s][1] = P->edge[b][s][0];
+            }
+    } else {
+        // export my 8 edge chunks, all-gather (pid, fds), fetch the neighbours' descriptors
+        constexpr int kW = 9;  // pid + [b][s][lo/hi] fds
+        std::vector<long long> mine(kW, -1), all((size_t)kW * g->world, -1);
+        mine[0] = (long long)getpid();
+        prctl(PR_SET_PTRACER, PR_SET_PTRACER_ANY, 0, 0, 0);  // let the peers' pidfd_getfd reach our fds
+        for (int b = 0; b < 2; ++b)
+            for (int s = 0; s < 2; ++s)
+                for (int e = 0; e < 2; ++e) {
+                    if (!u[s]) continue;
+                    int fd = -1;
+                    if (d.cuMemExportToShareableHandle(&fd, P->edge[b][s][e], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
+                                                       0) != CUDA_SUCCESS)
+                        return "cuMemExportToShareableHandle failed";
+                    mine[1 + (b * 2 + s) * 2 + e] = fd;
+                }
+        long long* dbuf = nullptr;
+        if (cudaMalloc(&dbuf, sizeof(long long) * kW * (g->world + 1)) != cudaSuccess) return "allocation failed";
+        ncclComm_t comm = (ncclComm_t)g->comm;
+        bool ok = cudaMemcpy(dbuf, mine.data(), sizeof(long long) * kW, cudaMemcpyHostToDevice) == cudaSuccess &&
+                  ncclAllGather(dbuf, dbuf + kW, kW, ncclInt64, comm, g->stream) == ncclSuccess &&
+                  cudaMemcpyAsync(all.data(), dbuf + kW, sizeof(long long) * kW * g->world, cudaMemcpyDeviceToHost,
+                                  g->stream) == cudaSuccess &&
+                  cudaStreamSynchronize(g->stream) == cudaSuccess;
+        if (!ok) {
+            cudaFree(dbuf);
+            return "all-gather of the exported chunk descriptors failed";
+        }
+        const int left = (g->rank + g->world - 1) % g->world, right = (g->rank + 1) % g->world;
+        std::vector<int> fetched;
+        auto import = [&](int peer, int b, int s, int e, CUmemGenericAllocationHandle* h) -> bool {
+            const long long* row = &all[(size_t)peer * kW];
+            int pfd = (int)syscall(SYS_pidfd_open, (pid_t)row[0], 0);
+            if (pfd < 0) return false;
+            int fd = (int)syscall(SYS_pidfd_getfd, pfd, (int)row[1 + (b * 2 + s) * 2 + e], 0);
+            close(pfd);
+            if (fd < 0) return false;
+            fetched.push_back(fd);
+            if (d.cuMemImportFromShareableHandle(h, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) !=
+                CUDA_SUCCESS)
+                return false;
+            P->handles.push_back(*h);
+            return true;
+        };
+        for (int b = 0; b < 2 && ok; ++b)
+            for (int s = 0; s < 2 && ok; ++s) {
+                if (!u[s]) continue;
+                ok = import(left, b, s, 1, &nb[b][s][0]) && import(right, b, s, 0, &nb[b][s][1]);
+            }
+        // nobody closes its exported descriptors before every rank has fetched them
+        int* flag = (int*)dbuf;
+        const bool bar = ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, comm, g->stream) == ncclSuccess &&
+                         cudaStreamSynchronize(g->stream) == cudaSuccess;
+        for (int fd : fetched) close(fd);
+        for (int i = 1; i < kW; ++i)
+            if (mine[i] >= 0) close((int)mine[i]);
+        cudaFree(dbuf);
+        if (!ok) return "importing a neighbour's chunk failed (pidfd_getfd / cuMemImportFromShareableHandle)";
+        if (!bar) return "barrier after the chunk exchange failed";
+        if (cudaMalloc(&P->d_fence, 4 * sizeof(int)) != cudaSuccess) return "allocation failed";
+        if (cudaMemset(P->d_fence, 0, 4 * sizeof(int)) != cudaSuccess) return "memset failed";
+    }
+    for (int b = 0; b < 2; ++b) {
+        size_t off = 0;
+        for (int s = 0; s < 2; ++s) {
+            if (!u[s]) continue;
+            const CUdeviceptr sec = P->base[b] + off;
+            if (!map(sec, p * u[s], nb[b][s][0]) || !map(sec + (nl + p) * u[s], p * u[s], nb[b][s][1]))
+                return "mapping a neighbour's edge chunk into the pad layers failed";
+            off += sec_bytes[s];
+        }
+        g->alloc[b] = (void*)P->base[b];
+    }
+    return "";
+}
+
+// world > 1: one send/recv of a word with both ring neighbours on the grid's stream
+cudaError_t peer_fence(sldg_grid g)
+{
+    if (g->world <= 1 || !g->peer) return cudaSuccess;
+    ncclComm_t comm = (ncclComm_t)g->comm;
+    const int left = (g->rank + g->world - 1) % g->world, right = (g->rank + 1) % g->world;
+    int* f = g->peer->d_fence;
+    bool ok = ncclGroupStart() == ncclSuccess && ncclSend(f, 1, ncclInt32, left, comm, g->stream) == ncclSuccess &&
+              ncclSend(f + 1, 1, ncclInt32, right, comm, g->stream) == ncclSuccess &&
+              ncclRecv(f + 2, 1, ncclInt32, left, comm, g->stream) == ncclSuccess &&
+              ncclRecv(f + 3, 1, ncclInt32, right, comm, g->stream) == ncclSuccess && ncclGroupEnd() == ncclSuccess;
+    return ok ? cudaSuccess : cudaErrorUnknown;
+}
+
+}  // namespace sldg

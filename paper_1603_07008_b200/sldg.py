@@ -31,7 +31,7 @@ EXPORTS = [
     "sldg_sweep_kernel", "sldg_vp_create", "sldg_vp_destroy", "sldg_vp_density", "sldg_vp_field",
     "sldg_vp_step", "sldg_transpose_plan", "sldg_transpose_count", "sldg_advect_vnodes",
     "sldg_advect_vnodes_device", "sldg_vp_set_nodal", "sldg_graph_begin", "sldg_graph_end",
-    "sldg_graph_launch", "sldg_graph_destroy",
+    "sldg_graph_launch", "sldg_graph_destroy", "sldg_peer_halo_check",
 ]
 
 
@@ -56,6 +56,7 @@ class Dist(ctypes.Structure):
 SLDG_DIST_FORCE_HALO = 1
 SLDG_DIST_FORCE_TRANSPOSE = 2
 SLDG_DIST_NCCL_SELF = 4
+SLDG_DIST_PEER_HALO = 8
 
 
 _lib = None
@@ -102,6 +103,7 @@ def lib():
         "sldg_layer_owner": [i64, ctypes.c_int, i64, ctypes.POINTER(ctypes.c_int), i64p],
         "sldg_transpose_plan": [i64, i64, ctypes.c_int, ctypes.c_int, i64p],
         "sldg_transpose_count": [vp, i64p],
+        "sldg_peer_halo_check": [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, i64],
         "sldg_advect_vnodes": [vp, ctypes.c_int, ctypes.c_int, dp],
         "sldg_advect_vnodes_device": [vp, ctypes.c_int, ctypes.c_int, vp],
         "sldg_vp_create": [vp, ctypes.c_int, ctypes.POINTER(vp)],
@@ -175,12 +177,26 @@ def layer_owner(n: int, world: int, layer: int):
     return o.value, loc.value
 
 
+def peer_halo_check(cells, k: int, precision: str, world: int, pad: int, gran: int = 2 << 20):
+    """sldg_peer_halo_check: None if SLDG_DIST_PEER_HALO accepts the layout, else the reason."""
+    cells = [int(c) for c in cells]
+    gd = GridDesc(len(cells), (ctypes.c_int64 * MAX_DIM)(*(cells + [1] * (MAX_DIM - len(cells)))))
+    prec = {"mixed": SLDG_MIXED, "fp64": SLDG_FP64}[precision]
+    st = lib().sldg_peer_halo_check(ctypes.byref(gd), int(k), prec, int(world), int(pad), int(gran))
+    if st == 0:
+        return None
+    if st == 5:
+        return lib().sldg_last_error().decode()
+    _check(st)
+
+
 class Grid:
     """Owns one sldg_grid handle.  Method names follow the C ABI (sldg_<name>)."""
 
     def __init__(self, cells, k: int, lo=None, hi=None, precision: str = "mixed",
                  rank: int = 0, world: int = 1, unique_id: bytes | None = None, max_halo: int = 0,
-                 force_halo: bool = False, force_transpose: bool = False, nccl_self: bool = False):
+                 force_halo: bool = False, force_transpose: bool = False, nccl_self: bool = False,
+                 peer_halo: bool = False):
         cells = [int(c) for c in cells]
         self.D = len(cells)
         self.cells = cells
@@ -200,13 +216,13 @@ class Grid:
             prec = {"mixed": SLDG_MIXED, "fp64": SLDG_FP64}[precision]
         dist_p = None
         self._uid = None
-        if world > 1 or force_halo or force_transpose or nccl_self:
+        if world > 1 or force_halo or force_transpose or nccl_self or peer_halo:
             uid = None
             if world > 1:
                 self._uid = ctypes.create_string_buffer(unique_id, 128)
                 uid = ctypes.cast(self._uid, ctypes.c_void_p)
             flags = ((SLDG_DIST_FORCE_HALO if force_halo else 0) | (SLDG_DIST_FORCE_TRANSPOSE if force_transpose else 0)
-                     | (SLDG_DIST_NCCL_SELF if nccl_self else 0))
+                     | (SLDG_DIST_NCCL_SELF if nccl_self else 0) | (SLDG_DIST_PEER_HALO if peer_halo else 0))
             self._dist = Dist(rank, world, uid, None, max_halo, flags)
             dist_p = ctypes.byref(self._dist)
         h = ctypes.c_void_p()
