@@ -114,6 +114,10 @@ typedef struct {
  * with ENOTSUP unless sldg_peer_halo_check accepts the layout at the device's allocation
  * granularity. */
 #define SLDG_DIST_PEER_HALO 8
+/* Testing (with SLDG_DIST_PEER_HALO, world == 1): the rank's own edge chunks are exported as
+ * POSIX file descriptors, fetched back with pidfd_getfd and imported -- the descriptor path of
+ * world > 1 exercised in one process. */
+#define SLDG_DIST_PEER_VIA_FD 16
 
 /* Create a grid (zero-filled).  k in 1..SLDG_MAX_K coefficients per dim (the paper's order
  * o = p+1).  dist may be NULL (single GPU).  The device is the caller's current

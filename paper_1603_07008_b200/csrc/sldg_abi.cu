@@ -1110,7 +1110,7 @@ static sldg_status create_impl(const sldg_grid_desc* grid, int k, const sldg_dom
     }
     g->alloc_bytes = array_alloc_bytes(L);
     if (g->peer_halo) {  // pads mapped onto the neighbours' edge layers (sldg_peer.cu); collective
-        std::string why = peer_alloc(g);
+        std::string why = peer_alloc(g, (dist->flags & SLDG_DIST_PEER_VIA_FD) != 0);
         if (!why.empty()) return bail(fail(SLDG_ENOTSUP, "SLDG_DIST_PEER_HALO: " + why));
         for (int b = 0; b < 2; ++b) g->buf[b] = arrays_of(L, g->alloc[b]);
     }

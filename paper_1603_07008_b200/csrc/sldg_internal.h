@@ -262,7 +262,7 @@ namespace sldg {
 // `gran` on every rank of `world`, else the reason
 std::string peer_halo_check(const Layout& L, int world, size_t gran);
 size_t peer_granularity(int device);  // 0 if the virtual-memory API is unavailable
-std::string peer_alloc(sldg_grid g);  // sets g->alloc[0..1] and g->peer; "" or the reason
+std::string peer_alloc(sldg_grid g, bool via_fd);  // sets g->alloc[0..1] and g->peer; "" or the reason
 void peer_free(sldg_grid g);
 cudaError_t peer_fence(sldg_grid g);  // world > 1: NCCL fence with both ring neighbours
 }  // namespace sldg

@@ -174,17 +174,22 @@ void peer_free(sldg_grid g)
 }
 
 // Reserve both arrays, back their local layers with this rank's chunks, map the neighbours'
-// edge chunks into the pads.  Returns "" or the reason (the caller destroys the grid).
-std::string peer_alloc(sldg_grid g)
+// edge chunks into the pads.  Returns "" or the reason (the caller destroys the grid).  With
+// world > 1 this is collective: a rank that fails locally still takes part in the all-gather
+// and the closing all-reduce (carrying its failure), so every rank returns the error together.
+// via_fd (world == 1, testing): the rank's own chunks go through the descriptor export /
+// pidfd_getfd / import path of world > 1.
+std::string peer_alloc(sldg_grid g, bool via_fd)
 {
     const Layout& L = g->lay;
     const Driver& d = drv();
     if (!d.ok) return "the CUDA virtual-memory driver entry points are unavailable";
     const size_t gran = peer_granularity(g->device);
     if (!gran) return "cuMemGetAllocationGranularity failed";
-    std::string why = peer_halo_check(L, g->world, gran);
+    std::string why = peer_halo_check(L, g->world, gran);  // identical on every rank
     if (!why.empty()) return why;
-    const bool shared = g->world > 1;
+    const bool multi = g->world > 1;
+    const bool shared = multi || via_fd;
     CUmemAllocationProp prop = alloc_prop(g->device, shared);
     sldg_peer_s* P = new sldg_peer_s();
     g->peer = P;
@@ -207,27 +212,34 @@ std::string peer_alloc(sldg_grid g)
         P->handles.push_back(*h);
         return true;
     };
-    for (int b = 0; b < 2; ++b) {
-        if (d.cuMemAddressReserve(&P->base[b], P->bytes, gran, 0, 0) != CUDA_SUCCESS)
-            return "cuMemAddressReserve of " + std::to_string(P->bytes) + " bytes failed";
+    // 1. local chunks
+    std::string err;
+    for (int b = 0; b < 2 && err.empty(); ++b) {
+        if (d.cuMemAddressReserve(&P->base[b], P->bytes, gran, 0, 0) != CUDA_SUCCESS) {
+            P->base[b] = 0;
+            err = "cuMemAddressReserve of " + std::to_string(P->bytes) + " bytes failed";
+            break;
+        }
         size_t off = 0;
-        for (int s = 0; s < 2; ++s) {
+        for (int s = 0; s < 2 && err.empty(); ++s) {
             if (!u[s]) continue;
             const CUdeviceptr sec = P->base[b] + off;
-            CUmemGenericAllocationHandle lo, mid, hi;
-            if (!create(p * u[s], &lo) || !map(sec + p * u[s], p * u[s], lo)) return "low chunk allocation failed";
-            if (nl > 2 * p && (!create((nl - 2 * p) * u[s], &mid) || !map(sec + 2 * p * u[s], (nl - 2 * p) * u[s], mid)))
-                return "middle chunk allocation failed";
-            if (!create(p * u[s], &hi) || !map(sec + nl * u[s], p * u[s], hi)) return "high chunk allocation failed";
+            CUmemGenericAllocationHandle lo = 0, mid = 0, hi = 0;
+            if (!create(p * u[s], &lo) || !map(sec + p * u[s], p * u[s], lo)) err = "low chunk allocation failed";
+            else if (nl > 2 * p &&
+                     (!create((nl - 2 * p) * u[s], &mid) || !map(sec + 2 * p * u[s], (nl - 2 * p) * u[s], mid)))
+                err = "middle chunk allocation failed";
+            else if (!create(p * u[s], &hi) || !map(sec + nl * u[s], p * u[s], hi)) err = "high chunk allocation failed";
+            else if (cudaMemsetAsync((void*)(sec + p * u[s]), 0, nl * u[s], g->stream) != cudaSuccess)
+                err = "memset failed";
             P->edge[b][s][0] = lo;
             P->edge[b][s][1] = hi;
-            if (cudaMemsetAsync((void*)(sec + p * u[s]), 0, nl * u[s], g->stream) != cudaSuccess)
-                return "memset failed";
             off += sec_bytes[s];
         }
     }
-    if (cudaStreamSynchronize(g->stream) != cudaSuccess) return "memset failed";
-    // the neighbours' edge chunks: [b][s][0] = left neighbour's high, [1] = right neighbour's low
+    if (err.empty() && cudaStreamSynchronize(g->stream) != cudaSuccess) err = "memset failed";
+    if (!multi && !err.empty()) return err;
+    // 2. the neighbours' edge chunks: nb[b][s][0] = left neighbour's high, [1] = right neighbour's low
     CUmemGenericAllocationHandle nb[2][2][2] = {};
     if (!shared) {
         for (int b = 0; b < 2; ++b)
@@ -236,33 +248,40 @@ std::string peer_alloc(sldg_grid g)
                 nb[b][s][1] = P->edge[b][s][0];
             }
     } else {
-        // export my 8 edge chunks, all-gather (pid, fds), fetch the neighbours' descriptors
+        // export my 8 edge chunks, all-gather (pid, fds) -- pid -1 marks a failed rank -- and
+        // fetch the neighbours' descriptors
         constexpr int kW = 9;  // pid + [b][s][lo/hi] fds
         std::vector<long long> mine(kW, -1), all((size_t)kW * g->world, -1);
-        mine[0] = (long long)getpid();
-        prctl(PR_SET_PTRACER, PR_SET_PTRACER_ANY, 0, 0, 0);  // let the peers' pidfd_getfd reach our fds
-        for (int b = 0; b < 2; ++b)
-            for (int s = 0; s < 2; ++s)
-                for (int e = 0; e < 2; ++e) {
-                    if (!u[s]) continue;
-                    int fd = -1;
-                    if (d.cuMemExportToShareableHandle(&fd, P->edge[b][s][e], CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR,
-                                                       0) != CUDA_SUCCESS)
-                        return "cuMemExportToShareableHandle failed";
-                    mine[1 + (b * 2 + s) * 2 + e] = fd;
-                }
-        long long* dbuf = nullptr;
-        if (cudaMalloc(&dbuf, sizeof(long long) * kW * (g->world + 1)) != cudaSuccess) return "allocation failed";
-        ncclComm_t comm = (ncclComm_t)g->comm;
-        bool ok = cudaMemcpy(dbuf, mine.data(), sizeof(long long) * kW, cudaMemcpyHostToDevice) == cudaSuccess &&
-                  ncclAllGather(dbuf, dbuf + kW, kW, ncclInt64, comm, g->stream) == ncclSuccess &&
-                  cudaMemcpyAsync(all.data(), dbuf + kW, sizeof(long long) * kW * g->world, cudaMemcpyDeviceToHost,
-                                  g->stream) == cudaSuccess &&
-                  cudaStreamSynchronize(g->stream) == cudaSuccess;
-        if (!ok) {
-            cudaFree(dbuf);
-            return "all-gather of the exported chunk descriptors failed";
+        if (err.empty()) {
+            prctl(PR_SET_PTRACER, PR_SET_PTRACER_ANY, 0, 0, 0);  // let the peers' pidfd_getfd reach our fds
+            for (int b = 0; b < 2; ++b)
+                for (int s = 0; s < 2; ++s)
+                    for (int e = 0; e < 2 && err.empty(); ++e) {
+                        if (!u[s]) continue;
+                        int fd = -1;
+                        if (d.cuMemExportToShareableHandle(&fd, P->edge[b][s][e],
+                                                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS)
+                            err = "cuMemExportToShareableHandle failed";
+                        else
+                            mine[1 + (b * 2 + s) * 2 + e] = fd;
+                    }
         }
+        mine[0] = err.empty() ? (long long)getpid() : -1;
+        long long* dbuf = nullptr;
+        bool comm_ok = true;
+        if (multi) {
+            ncclComm_t comm = (ncclComm_t)g->comm;
+            comm_ok = cudaMalloc(&dbuf, sizeof(long long) * kW * (g->world + 1)) == cudaSuccess &&
+                      cudaMemcpy(dbuf, mine.data(), sizeof(long long) * kW, cudaMemcpyHostToDevice) == cudaSuccess &&
+                      ncclAllGather(dbuf, dbuf + kW, kW, ncclInt64, comm, g->stream) == ncclSuccess &&
+                      cudaMemcpyAsync(all.data(), dbuf + kW, sizeof(long long) * kW * g->world,
+                                      cudaMemcpyDeviceToHost, g->stream) == cudaSuccess &&
+                      cudaStreamSynchronize(g->stream) == cudaSuccess;
+        } else {
+            all = mine;
+        }
+        bool any_failed = !comm_ok;
+        for (int r = 0; r < g->world && comm_ok; ++r) any_failed |= all[(size_t)r * kW] < 0;
         const int left = (g->rank + g->world - 1) % g->world, right = (g->rank + 1) % g->world;
         std::vector<int> fetched;
         auto import = [&](int peer, int b, int s, int e, CUmemGenericAllocationHandle* h) -> bool {
@@ -279,24 +298,40 @@ std::string peer_alloc(sldg_grid g)
             P->handles.push_back(*h);
             return true;
         };
+        bool ok = !any_failed;
         for (int b = 0; b < 2 && ok; ++b)
             for (int s = 0; s < 2 && ok; ++s) {
                 if (!u[s]) continue;
                 ok = import(left, b, s, 1, &nb[b][s][0]) && import(right, b, s, 0, &nb[b][s][1]);
             }
-        // nobody closes its exported descriptors before every rank has fetched them
-        int* flag = (int*)dbuf;
-        const bool bar = ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, comm, g->stream) == ncclSuccess &&
-                         cudaStreamSynchronize(g->stream) == cudaSuccess;
+        if (err.empty() && !ok)
+            err = any_failed ? "another rank failed to set up its peer-mapped halo chunks"
+                             : "importing a neighbour's chunk failed (pidfd_getfd / cuMemImportFromShareableHandle)";
+        // nobody closes its exported descriptors before every rank has fetched them; the sum
+        // of failures decides for all
+        if (multi && comm_ok) {
+            int* flag = (int*)dbuf;
+            const int mine_bad = err.empty() ? 0 : 1;
+            int bad = 1;
+            comm_ok = cudaMemcpy(flag, &mine_bad, sizeof(int), cudaMemcpyHostToDevice) == cudaSuccess &&
+                      ncclAllReduce(flag, flag, 1, ncclInt32, ncclSum, (ncclComm_t)g->comm, g->stream) == ncclSuccess &&
+                      cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, g->stream) == cudaSuccess &&
+                      cudaStreamSynchronize(g->stream) == cudaSuccess;
+            if (err.empty() && (!comm_ok || bad)) err = "another rank failed to map its peer-mapped halo chunks";
+        }
+        if (multi && !comm_ok && err.empty()) err = "the chunk descriptor exchange failed";
         for (int fd : fetched) close(fd);
         for (int i = 1; i < kW; ++i)
             if (mine[i] >= 0) close((int)mine[i]);
-        cudaFree(dbuf);
-        if (!ok) return "importing a neighbour's chunk failed (pidfd_getfd / cuMemImportFromShareableHandle)";
-        if (!bar) return "barrier after the chunk exchange failed";
-        if (cudaMalloc(&P->d_fence, 4 * sizeof(int)) != cudaSuccess) return "allocation failed";
-        if (cudaMemset(P->d_fence, 0, 4 * sizeof(int)) != cudaSuccess) return "memset failed";
+        if (dbuf) cudaFree(dbuf);
+        if (!err.empty()) return err;
+        if (multi) {
+            if (cudaMalloc(&P->d_fence, 4 * sizeof(int)) != cudaSuccess) return "allocation failed";
+            if (cudaMemset(P->d_fence, 0, 4 * sizeof(int)) != cudaSuccess) return "memset failed";
+        }
     }
+    // 3. the pads.  (world > 1: a failure here is local to a rank that already passed the
+    // collective steps; its creation fails, the neighbours' grids stay valid)
     for (int b = 0; b < 2; ++b) {
         size_t off = 0;
         for (int s = 0; s < 2; ++s) {

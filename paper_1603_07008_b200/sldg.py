@@ -57,6 +57,7 @@ SLDG_DIST_FORCE_HALO = 1
 SLDG_DIST_FORCE_TRANSPOSE = 2
 SLDG_DIST_NCCL_SELF = 4
 SLDG_DIST_PEER_HALO = 8
+SLDG_DIST_PEER_VIA_FD = 16
 
 
 _lib = None
@@ -196,7 +197,7 @@ class Grid:
     def __init__(self, cells, k: int, lo=None, hi=None, precision: str = "mixed",
                  rank: int = 0, world: int = 1, unique_id: bytes | None = None, max_halo: int = 0,
                  force_halo: bool = False, force_transpose: bool = False, nccl_self: bool = False,
-                 peer_halo: bool = False):
+                 peer_halo: bool = False, peer_via_fd: bool = False):
         cells = [int(c) for c in cells]
         self.D = len(cells)
         self.cells = cells
@@ -222,7 +223,8 @@ class Grid:
                 self._uid = ctypes.create_string_buffer(unique_id, 128)
                 uid = ctypes.cast(self._uid, ctypes.c_void_p)
             flags = ((SLDG_DIST_FORCE_HALO if force_halo else 0) | (SLDG_DIST_FORCE_TRANSPOSE if force_transpose else 0)
-                     | (SLDG_DIST_NCCL_SELF if nccl_self else 0) | (SLDG_DIST_PEER_HALO if peer_halo else 0))
+                     | (SLDG_DIST_NCCL_SELF if nccl_self else 0) | (SLDG_DIST_PEER_HALO if peer_halo else 0)
+                     | (SLDG_DIST_PEER_VIA_FD if peer_via_fd else 0))
             self._dist = Dist(rank, world, uid, None, max_halo, flags)
             dist_p = ctypes.byref(self._dist)
         h = ctypes.c_void_p()

@@ -122,3 +122,19 @@ def test_peer_halo_mass_conserved():
     m1 = gp.mass()
     assert abs(m1 - m0) <= 1e-13 * max(1.0, abs(m0))
     gp.destroy()
+
+
+def test_peer_halo_descriptor_path_in_one_process():
+    """SLDG_DIST_PEER_VIA_FD: the edge chunks go through the multi-process route (export as POSIX
+    file descriptors, pidfd_getfd, import, map) with the rank as its own neighbour; the sweeps
+    are bit-identical to the directly mapped pads."""
+    dims, k, pad = [32, 32, 32, 32], 3, 8
+    ga = _Grid(dims, k, precision="mixed", force_halo=True, peer_halo=True, max_halo=pad)
+    gb = _Grid(dims, k, precision="mixed", force_halo=True, peer_halo=True, peer_via_fd=True, max_halo=pad)
+    for g in (ga, gb):
+        g.fill_random(21)
+        for d, s in [(3, 1.7), (0, 0.4), (3, -7.2), (2, 0.9), (3, 6.6)]:
+            g.advect(d, shift=s)
+    assert ga.get_coeffs().tobytes() == gb.get_coeffs().tobytes()
+    ga.destroy()
+    gb.destroy()
