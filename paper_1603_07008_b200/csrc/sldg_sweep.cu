@@ -440,7 +440,7 @@ const char* sweep_kernel_name(const Layout& lay, const Sweep& sw)
     if (lay.D == 1 && (!(e && e[0] == 'r') || lay.prec == SLDG_GENERAL)) return line_kernel_name(lay);
     TmaPlan pl;
     const bool tma = !(e && e[0] == 'r') && tma_plan(lay, sw, &pl);
-    if (sw.dim == 0) return tma ? "sweep_d0_tma" : "sweep_d0_kernel";
+    if (sw.dim == 0) return tma ? (pl.T > 0 ? "sweep_d0_win" : "sweep_d0_tma") : "sweep_d0_kernel";
     return tma ? "sweep_strided_tma" : "sweep_strided_kernel";
 }
 

@@ -1064,6 +1064,161 @@ __global__ void __launch_bounds__(kTmaThreads, MINB) sweep_d0_tma(Layout lay, Sw
 }
 
 // ============================================================================================
+// d = 0 for lines too long for two whole-line stages (fp64 k >= 4, mixed k >= 7 at n0 = 4096):
+// tile = one WINDOW of cw = pl.T consecutive targets [a, a + cw) of one line (R = 1).  By
+// P:259-272 target i reads cells i - i* - 1 and i - i*, so the window's sources are the cw + 1
+// cells from ws = (a - i* - 1) mod n0 -- rounded down to a multiple of 4 cells (rofs) so every
+// copy is 16-byte aligned -- loaded per plane as one 1D bulk copy, two where the periodic line
+// wraps.  The producer reads i* mod n0 of the line (Weights::smod) at the tile's first stage;
+// the consumers take it from the line record and compute the same rofs, and a target's source
+// columns are then (target - a) + rofs + r: no modulo.  Stage layout as sweep_d0_tma (slot
+// stride pl.Rmax cells, the line record at the end); the consumer code is the same d0_consume.
+// ============================================================================================
+template <int KK, int PREC>
+__global__ void __launch_bounds__(kTmaThreads, 1) sweep_d0_win(Layout lay, Sweep sw, Arrays src, Arrays dst, int64_t lb,
+                                                          int64_t le, TmaPlan pl)
+{
+    extern __shared__ __align__(128) unsigned char smem[];
+    const int S = pl.stages;
+    uint64_t* full = (uint64_t*)smem;
+    uint64_t* empty = full + S;
+    unsigned char* stage0 = smem + 256;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int NC = kTmaConsumerWarps;
+    const bool producer = (warp == NC);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < S; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+    pdl_wait();  // the weights and the source array come from the preceding kernels
+
+    const int D = lay.D;
+    const int n0 = (int)lay.n[0];
+    const int64_t L = lay.L;
+    const int cw = pl.T;                       // targets per window
+    const int cs = pl.Rmax;                    // stage slot stride (cells)
+    const int nwin = (n0 + cw - 1) / cw;
+    const int64_t lines_per_layer = L / n0;
+    const int64_t nblk = lines_per_layer * nwin;
+    const int64_t ntiles = nblk * (le - lb);
+    const int G = lay.K / KK, GC = pl.GC;
+    const int BP = GC * KK;
+    const int NQ = NC * 32 * kD0Tpt;
+    const uint64_t pol = policy_evict_first();
+    const int recw = 2 * KK * KK + 2;
+    const int rec_off = pl.stage_bytes - recw * 8;
+    constexpr bool SMW = KK > kD0RegK;
+    const int q4 = (int)threadIdx.x * kD0Tpt;
+    uint32_t it = 0;
+    int64_t my_s = 0;
+    int my_cp = 0;
+    double wr[SMW ? 1 : 2 * KK * KK];
+    int64_t f = 0;            // producer: field entry of the tile's line
+    int ws = 0, p1 = 0, p2 = 0;  // producer: window start (cells) and its two pieces
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (tile + gridDim.x >= ntiles) pdl_trigger();  // this CTA's last tile
+        const int64_t blk = tile % nblk;
+        const int64_t layer = lb + tile / nblk;
+        const int64_t layerp = lay.pad + layer;
+        const int64_t line = blk / nwin;
+        const int a = (int)(blk - line * nwin) * cw;
+        const int ct = (n0 - a < cw) ? n0 - a : cw;  // targets in this window (multiple of 4)
+        const int64_t line_base = line * n0;
+        for (int g0 = 0; g0 < G; g0 += GC) {
+            const int gc = (G - g0) < GC ? (G - g0) : GC;
+            const int s = it % S;
+            const uint32_t ph = (it / S) & 1;
+            ++it;
+            unsigned char* st = stage0 + (size_t)s * pl.stage_bytes;
+            const bool massg = (PREC == SLDG_MIXED) && g0 == 0;
+            if (producer) {
+                if (lane == 0) {
+                    if (g0 == 0) {
+                        f = 0;
+                        if (sw.fmask) {
+                            int64_t idx[kMaxDim];
+                            int64_t rem = line;
+#pragma unroll
+                            for (int e = 0; e < kMaxDim; ++e) idx[e] = 0;
+                            for (int e = 1; e < D - 1; ++e) {
+                                idx[e] = rem % lay.n[e];
+                                rem /= lay.n[e];
+                            }
+                            if (D >= 2) idx[D - 1] = lay.first_layer + layer;
+                            f = tfield_index(sw, idx, D);
+                        }
+                        int w0 = a - (int)__ldg(&sw.smod[f]) - 1;  // A-source of target a, mod n0
+                        if (w0 < 0) w0 += n0;
+                        const int rofs = w0 & 3;
+                        ws = w0 - rofs;
+                        const int cnt = (ct + 1 + rofs + 3) & ~3;
+                        p1 = (cnt < n0 - ws) ? cnt : n0 - ws;
+                        p2 = cnt - p1;
+                    }
+                    mbar_wait(&empty[s], ph ^ 1);
+                    const uint32_t es = (PREC == SLDG_FP64) ? 8u : 4u;
+                    const uint32_t cb = (uint32_t)(p1 + p2);
+                    uint32_t bytes = cb * (massg ? (BP - 1) * 4u + 8u : (uint32_t)gc * KK * es);
+                    if (g0 == 0 || SMW) bytes += (uint32_t)(recw * 8);
+                    mbar_expect_tx(&full[s], bytes);
+                    unsigned char* dp = st;
+                    for (int j = 0; j < gc * KK; ++j) {
+                        const int q = g0 * KK + j;
+                        const uint32_t ej = (PREC == SLDG_FP64 || (massg && j == 0)) ? 8u : 4u;
+                        const char* sp = slot_ptr<PREC>(src, lay, q, layerp, line_base);
+                        bulk_g2s(dp, sp + (size_t)ws * ej, (uint32_t)p1 * ej, &full[s], pol);
+                        if (p2) bulk_g2s(dp + (size_t)p1 * ej, sp, (uint32_t)p2 * ej, &full[s], pol);
+                        dp += (size_t)cs * ej;
+                    }
+                    if (g0 == 0 || SMW) bulk_g2s(st + rec_off, sw.rec + f * recw, (uint32_t)(recw * 8), &full[s], pol);
+                }
+                __syncwarp();
+            } else {
+                mbar_wait(&full[s], ph);
+                const double* rp = (const double*)(st + rec_off);
+                if (g0 == 0) {
+                    if (!SMW) {
+#pragma unroll
+                        for (int i = 0; i < 2 * KK * KK; ++i) wr[i] = rp[i];
+                    }
+                    my_s = __double_as_longlong(rp[2 * KK * KK]);
+                    my_cp = (int)__double_as_longlong(rp[2 * KK * KK + 1]);
+                }
+                int w0 = a - (int)my_s - 1;
+                if (w0 < 0) w0 += n0;
+                const int rofs = w0 & 3;
+                for (int cc = q4; cc < ct; cc += NQ) {
+                    int col[kD0Tpt + 1];
+#pragma unroll
+                    for (int r = 0; r <= kD0Tpt; ++r) col[r] = cc + rofs + r;
+                    const int64_t tin = line_base + a + cc;
+                    const int q0 = g0 * KK;
+                    double* om;
+                    float* of = nullptr;
+                    if (PREC == SLDG_FP64) {
+                        om = dst.s64 + toff_m<PREC>(lay, layerp, tin) + (int64_t)q0 * L;
+                    } else {
+                        om = dst.mass + toff_m<PREC>(lay, layerp, tin);
+                        of = dst.pl + toff_f<PREC>(lay, layerp, tin) + (massg ? 0 : (int64_t)(q0 - 1) * L);
+                    }
+                    const double* wsrc = SMW ? rp : wr;
+                    if (massg)
+                        d0_consume<KK, PREC, true>(st, gc, cs, col, om, of, L, my_cp, wsrc);
+                    else
+                        d0_consume<KK, PREC, false>(st, gc, cs, col, om, of, L, my_cp, wsrc);
+                }
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+        }
+    }
+}
+
+// ============================================================================================
 // planning, tensor maps, launch
 // ============================================================================================
 static int g_num_sms = 0;
@@ -1187,9 +1342,10 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
     // threads per column with half the output slots each); k >= 7 uses the register kernels.
     // d = 0: k <= 4 in registers, 5..8 from the record in shared memory (kD0RegK)
     if (k > 8 || (k > 6 && sw.dim != 0)) return false;
-    // fp64 k = 5, 6 strided: the register kernel is faster (C3: 1.12 / 1.59 ms vs 1.25 / 1.82 ms
-    // split TMA, whose two threads per column both read every fp64 input row)
-    if (k > 4 && sw.dim != 0 && lay.prec == SLDG_FP64) return false;
+    // fp64 k = 5, 6 strided: the split TMA kernel (round 2, C3 4096^2: 1.26 / 1.78 ms against the
+    // register kernel's 2.08 / 4.89 ms; profiles/round2/d0win ab_*); SLDG_TMA_F64HI=0 selects the latter
+    if (k > 4 && sw.dim != 0 && lay.prec == SLDG_FP64 && getenv("SLDG_TMA_F64HI") && atoi(getenv("SLDG_TMA_F64HI")) == 0)
+        return false;
     if (n0 % 4 != 0) return false;
     const int64_t layers_alloc = lay.layers + 2 * lay.pad;
     if (lay.L > (int64_t)1 << 31 || layers_alloc > 65535) return false;
@@ -1198,15 +1354,49 @@ static bool tma_plan_ctas(const Layout& lay, const Sweep& sw, TmaPlan* pl, int f
         const int64_t NQ = (int64_t)NT * 4;
         const int64_t lines = lay.L / n0;
         int64_t R = (n0 <= NQ) ? std::min<int64_t>(NQ / n0, lines) : 1;
+        // lines too long for two whole-line stages (or whose length is not a multiple of 16
+        // cells): windows of cw targets (sweep_d0_win), one group per stage, the fewest windows
+        // per line whose two stages fit the opt-in carveout
+        auto try_win = [&]() -> bool {
+            if (ctas != 1 || n0 < 64) return false;
+            const int es = (lay.prec == SLDG_FP64) ? 8 : 4;
+            const int64_t recb = (int64_t)(2 * k * k + 2) * 8;
+            const int64_t budget_max = (int64_t)g_smem_optin - 256;
+            for (int nwin = 2; nwin <= 64; nwin *= 2) {
+                const int64_t cw = ((n0 + nwin - 1) / nwin + 3) / 4 * 4;
+                const int64_t wcs = (cw + 8 + 15) / 16 * 16;  // cw + 1 sources + rofs <= 3, rounded to 4
+                const int64_t sb = ((wcs * (k * es + ((lay.prec == SLDG_FP64) ? 0 : 4)) + 127) / 128 * 128 + recb + 127) /
+                                   128 * 128;
+                if (2 * sb > budget_max) continue;
+                pl->R = 1;
+                pl->GC = 1;
+                pl->rec1 = 1;
+                pl->T = (int)cw;
+                pl->Rmax = (int)wcs;
+                pl->stage_bytes = (int)sb;
+                pl->stages = (int)std::min<int64_t>(8, std::max<int64_t>(2, budget / sb));
+                if ((int64_t)pl->stages * sb > budget_max) pl->stages = 2;
+                return true;
+            }
+            return false;
+        };
+        // windows also for long mixed k >= 6 lines (C3 k = 6: 1.23 vs 1.29 ms whole-line; slower for
+        // k <= 5: 0.14 / 0.25 / 0.46 / 0.84 vs 0.125 / 0.22 / 0.43 / 0.82 ms, profiles/round2/d0win ab_*);
+        // SLDG_D0_WIN=1 / 0 forces / forbids them where both apply
+        {
+            const char* e = getenv("SLDG_D0_WIN");
+            const bool want_win = e ? atoi(e) == 1 : (k >= 6);
+            if (n0 > NQ && want_win && try_win()) return true;
+        }
         while (R > 1 && (R * n0) % 16 != 0) --R;  // stage slots stay 64-byte multiples
-        if ((R * n0) % 16 != 0) return false;
+        if ((R * n0) % 16 != 0) return n0 > NQ ? try_win() : false;
         const int64_t cs = R * n0;
         const int64_t group_bytes = cs * bpc_max;  // one coupled group of the tile, worst case
         const int G = lay.K / k;
         int64_t d0div = (k <= 2) ? 2 : 3;  // stage <= budget / d0div (C4: 2 beats 3, 3.8 -> 4.1 TB/s; override SLDG_TMA_D0DIV)
         if (const char* e = getenv("SLDG_TMA_D0DIV")) d0div = atoi(e);
         const int64_t target = budget / d0div;
-        if (group_bytes > std::max<int64_t>(budget, (int64_t)g_smem_optin / ctas - 256) / 2) return false;
+        if (group_bytes > std::max<int64_t>(budget, (int64_t)g_smem_optin / ctas - 256) / 2) return try_win();
         int gcmax = (int)std::max<int64_t>(1, std::min<int64_t>(G, target / group_bytes));
         const int nchunk = (G + gcmax - 1) / gcmax;
         const int GC = (G + nchunk - 1) / nchunk;  // balanced chunks
@@ -1450,9 +1640,18 @@ template <int KK, int PREC>
 static cudaError_t launch_tma_k(const Layout& lay, const Sweep& sw, const Arrays& src, const Arrays& dst, int64_t lb,
                                 int64_t le, const TmaPlan& pl, cudaStream_t s)
 {
+    const size_t smem = 256 + (size_t)pl.stages * pl.stage_bytes;
+    if (sw.dim == 0 && pl.T > 0) {  // windowed d = 0 (no tensor maps: 1D bulk copies)
+        const int64_t nwin = (lay.n[0] + pl.T - 1) / pl.T;
+        const int64_t ntw = (lay.L / lay.n[0]) * nwin * (le - lb);
+        auto kern = sweep_d0_win<KK, PREC>;
+        ensure_max_smem((const void*)kern);
+        int64_t grid = std::min<int64_t>(ntw, (int64_t)std::max(1, g_num_sms - sw.sm_reserve));
+        if (grid < 1) return cudaSuccess;
+        return launch_pdl(kern, dim3((unsigned)grid), dim3(kTmaThreads), smem, s, lay, sw, src, dst, lb, le, pl);
+    }
     TmapSet tmaps;
     if (!cached_tmaps(lay, sw, src, pl, &tmaps)) return cudaErrorInvalidValue;
-    const size_t smem = 256 + (size_t)pl.stages * pl.stage_bytes;
     int64_t ntiles;
     const int per_sm = pl.ctas;  // CTAs per SM the plan sized shared memory for
     if (sw.dim == 0) {

@@ -740,17 +740,17 @@ def test_randomized_medium_grids_match_oracle(seed):
 @pytest.mark.parametrize("dims,k", [([64, 20], 5), ([48, 6, 5], 6), ([16, 4, 3], 7), ([12, 4, 3], 8),
                                     ([4096, 6], 5), ([20, 6, 4, 3], 5), ([1024, 9], 6)])
 def test_high_order_d0_tma_matches_oracle(dims, k, precision):
-    if dims[0] == 4096 and precision == "fp64":
-        pytest.skip("two stages of a 4096-cell fp64 k = 5 group exceed shared memory (register kernel)")
     """k = 5..8 on d = 0: the TMA kernel reading the line weights from the record in shared memory
     (a copy in every stage of the tile); constant shifts, per-line fields (one record per tile
-    and one per line) and copy lines."""
+    and one per line) and copy lines.  A 4096-cell fp64 k = 5 line does not fit two whole-line
+    stages: the windowed kernel (sweep_d0_win) runs it."""
     D, K = len(dims), k ** len(dims)
     rng = np.random.default_rng(77 + k)
     c = sldg_inputs.random_coeffs(dims, k, 5150 + k)
     ref_in = oracle_input(c, K, precision)
     g = _Grid(dims, k, precision=precision)
-    assert g.sweep_kernel(0) == "sweep_d0_tma", g.sweep_kernel(0)
+    want = "sweep_d0_win" if (dims[0] == 4096 and precision == "fp64") else "sweep_d0_tma"
+    assert g.sweep_kernel(0) == want, g.sweep_kernel(0)
     cases = [(3.37, None, 0), (-0.41 - dims[0], None, 0)]
     if D >= 2:
         mask = (1 << (D - 1)) | (2 if D >= 3 else 0)
@@ -780,8 +780,7 @@ def test_high_order_strided_tma_matches_oracle(dims, k, precision):
     ref_in = oracle_input(c, K, precision)
     g = _Grid(dims, k, precision=precision)
     for dim in range(1, D):
-        want = "sweep_strided_tma" if precision == "mixed" else "sweep_strided_kernel"  # fp64: register kernel
-        assert g.sweep_kernel(dim) == want, (dim, g.sweep_kernel(dim))
+        assert g.sweep_kernel(dim) == "sweep_strided_tma", (dim, g.sweep_kernel(dim))
         f0 = rng.uniform(-3.2, 3.2, dims[0])
         f0[::6] = np.round(f0[::6])
         cases = [(2.37, None, 0), (-0.63 - dims[dim], None, 0), (0.0, f0, 1)]
@@ -822,4 +821,39 @@ def test_host_field_not_retained(precision):
         ref = oracle.round_layout(oracle.advect(ref, dims, k, 1, field=f, field_mask=1, n_double=n_double(precision, K)),
                                   K, n_double(precision, K))
     assert_parity(got, ref, K, precision, "host field clobbered after sldg_advect", ref_in, 1, k)
+    g.destroy()
+
+
+@pytest.mark.parametrize("dims,k,precision", [([4096, 3], 4, "fp64"), ([4100, 2], 4, "fp64"), ([4100, 3], 3, "mixed"), ([4096, 2, 2], 6, "fp64"),
+                                              ([2048, 3], 8, "fp64"), ([4096, 2], 6, "mixed"), ([4096, 2], 7, "mixed"), ([4096, 2], 8, "mixed"),
+                                              ([8192, 2], 4, "fp64")])
+def test_windowed_d0_matches_oracle(dims, k, precision):
+    """d = 0 lines too long for two whole-line stages (sweep_d0_win): tiles are windows of cw
+    targets whose cw + 1 sources start at (a - i* - 1) mod n0, loaded as one or two
+    (periodic wrap) bulk copies per plane.  Shifts that put the window across the wrap at every
+    offset mod 4, negative and multi-line shifts, integer shifts (copy lines) and per-line
+    fields; a ragged last window (n0 = 4100)."""
+    D, K = len(dims), k ** len(dims)
+    rng = np.random.default_rng(31 * k + D)
+    c = sldg_inputs.random_coeffs(dims, k, 7100 + k)
+    ref_in = oracle_input(c, K, precision)
+    g = _Grid(dims, k, precision=precision)
+    assert g.sweep_kernel(0) == "sweep_d0_win", g.sweep_kernel(0)
+    n0 = dims[0]
+    cases = [(0.37, None, 0), (1.5, None, 0), (2.61, None, 0), (3.99, None, 0), (-0.41, None, 0),
+             (-n0 / 2 - 0.3, None, 0), (2.5 * n0 + 0.77, None, 0), (5.0, None, 0), (-3.0, None, 0)]
+    mask = (1 << (D - 1)) | (2 if D >= 3 else 0)
+    nf = int(np.prod([dims[e] for e in range(D) if mask >> e & 1]))
+    field = rng.uniform(-2.5 * n0, 2.5 * n0, nf)
+    field[::3] = np.round(field[::3])
+    cases.append((0.0, field, mask))
+    for shift, field, mask in cases:
+        g.set_coeffs(c)
+        g.advect(0, shift=shift, field=field, field_mask=mask)
+        got = g.get_coeffs()
+        ref = oracle.advect(ref_in, dims, k, 0, shift=shift, field=field, field_mask=mask,
+                            n_double=n_double(precision, K))
+        if field is None and shift == round(shift):
+            assert got.tobytes() == ref.tobytes()  # integer shift: an exact rotation
+        assert_parity(got, ref, K, precision, f"dims={dims} k={k} nu={shift} mask={mask}", ref_in, 0, k)
     g.destroy()
