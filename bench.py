@@ -664,7 +664,7 @@ def time_vlasov(g, stream, dims, kinds, k, steps=3, dt=0.1):
     vp.destroy()
     nodal = {"ms_per_step": nodal_ms, "x_sweep_kernel_ms": v_ms / max(1, v_n),
              "x_sweep_gbs": (v_bytes / (v_ms * 1e-3) / 1e9) if v_ms else None,
-             "x_sweep_kernel": "vnode_sweep_kernel (Gauss-node x1 sweep, V7)"}
+             "x_sweep_kernel": "vnode_sweep_multi (Gauss-node x1 sweep, V7; 2 cells per thread)"}
     return {"ms_per_step": step_ms, "nodal_x": nodal, "sweeps_per_step": 3 * dx, "density_and_field_ms": field_ms,
             "field_share_of_step": field_ms / step_ms,
             "gdofs_per_sweep": 3 * dx * cells * K / (step_ms * 1e-3) / 1e9,

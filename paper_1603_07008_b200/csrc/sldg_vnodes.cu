@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "sldg_basis.cuh"
 #include "sldg_internal.h"
@@ -155,9 +156,9 @@ __global__ void __launch_bounds__(256, KK <= 3 ? 4 : 3) vnode_sweep_kernel(Layou
     const int nofs = (int)__double_as_longlong(__ldg(&r[1]));
     if (uni) {
         const double* M0 = rec + j0 * vn_rec_words(KK) + 2;
-        for (int x = threadIdx.x; x < kVnMaxOfs * K4; x += blockDim.x) {
+        for (int x = threadIdx.x; x < kVnMaxOfs * K4; x += blockDim.x) {  // transposed: [o][l][m]
             const int o = x / K4, rem = x - o * K4, m = rem / K2, l = rem - m * K2;
-            sM[(o * K2 + m) * RS + l] = __ldg(&M0[x]);
+            sM[(o * K2 + l) * RS + m] = __ldg(&M0[x]);
         }
         if (RS != K2)
             for (int x = threadIdx.x; x < kVnMaxOfs * K2; x += blockDim.x) sM[x * RS + K2] = 0.0;
@@ -230,17 +231,17 @@ __global__ void __launch_bounds__(256, KK <= 3 ? 4 : 3) vnode_sweep_kernel(Layou
             }
             if (RS != K2) v[K2] = 0.0;
             if (uni) {
+                // outer product over l: K2 independent accumulator chains (each out[m] still sums
+                // over l = 0, 1, ... in order)
                 const double* Mo = sM + o * K2 * RS;
 #pragma unroll
-                for (int m = 0; m < K2; ++m) {
-                    double acc = out[m];
+                for (int l = 0; l < K2; ++l) {
 #pragma unroll
-                    for (int l = 0; l < RS; l += 2) {
-                        const double2 mm = *(const double2*)&Mo[m * RS + l];
-                        acc = fma(mm.x, v[l], acc);
-                        if (l + 1 < K2) acc = fma(mm.y, v[l + 1], acc);
+                    for (int m = 0; m < RS; m += 2) {
+                        const double2 mm = *(const double2*)&Mo[l * RS + m];
+                        out[m] = fma(mm.x, v[l], out[m]);
+                        if (m + 1 < K2) out[m + 1] = fma(mm.y, v[l], out[m + 1]);
                     }
-                    out[m] = acc;
                 }
             } else {
                 const double* Mo = M + o * K4;
@@ -268,6 +269,136 @@ __global__ void __launch_bounds__(256, KK <= 3 ? 4 : 3) vnode_sweep_kernel(Layou
     }
 }
 
+// Round 2 (NEXT-3 speed): CPT consecutive cells per thread.  Taken when the CTA's 256 CPT cells
+// share their v-cell (S_e a multiple of 256 CPT) and d is not the layer dim, so M_o always comes
+// from shared memory and every 16-byte M read serves CPT cells (the one-cell kernel spends most
+// of its issue slots and L1 bandwidth on those reads: profiles/round1/ncu_full_vnode_c5s.md).
+// The source offset of cell c at offset o is one int32 delta (cells) from the cell itself; the
+// offset loop is unrolled to kVnMaxOfs with guards, so deltas and accumulators stay in registers.
+// Same operation order per output as vnode_sweep_kernel: results are bit-identical.
+template <int KK, int CPT>
+__global__ void __launch_bounds__(256, KK <= 3 ? 2 : 1) vnode_sweep_multi(Layout lay, int d, int e, const double* __restrict__ rec,
+                                                            Arrays src, Arrays dst)
+{
+    constexpr int K2 = KK * KK, K4 = K2 * K2;
+    constexpr int RS = (K2 + 1) & ~1;
+    extern __shared__ __align__(16) double sM[];  // [kVnMaxOfs][K2][RS]
+    const int D = lay.D;
+    const int64_t cta0 = (int64_t)blockIdx.x * blockDim.x * CPT;
+    const int64_t t0 = cta0 + (int64_t)threadIdx.x * CPT;
+    auto idx_of = [&](int dd, int64_t lay_, int64_t in_) -> int64_t {
+        if (dd == D - 1) return lay.first_layer + lay_;
+        return (in_ / lay.S[dd]) % lay.n[dd];
+    };
+    const int64_t l0 = cta0 / lay.L;
+    const int64_t j = idx_of(e, l0, cta0 - l0 * lay.L);  // the CTA's v-cell
+    const double* r = rec + j * vn_rec_words(KK);
+    const int64_t omin = (int64_t)__double_as_longlong(__ldg(&r[0]));
+    const int nofs = (int)__double_as_longlong(__ldg(&r[1]));
+    {
+        const double* M0 = r + 2;
+        for (int x = threadIdx.x; x < kVnMaxOfs * K4; x += blockDim.x) {  // transposed: [o][l][m]
+            const int o = x / K4, rem = x - o * K4, m = rem / K2, l = rem - m * K2;
+            sM[(o * K2 + l) * RS + m] = __ldg(&M0[x]);
+        }
+        if (RS != K2)
+            for (int x = threadIdx.x; x < kVnMaxOfs * K2; x += blockDim.x) sM[x * RS + K2] = 0.0;
+        __syncthreads();
+    }
+    if (t0 >= lay.cells) return;
+    const int64_t layer = t0 / lay.L, inner = t0 - layer * lay.L;
+    const int64_t lp = lay.pad + layer;
+    const int64_t nd = lay.n[d];
+    const int64_t id0 = idx_of(d, layer, inner);
+    int dl[CPT][kVnMaxOfs];  // source cell of (cell c, offset o) relative to cell c
+#pragma unroll
+    for (int c = 0; c < CPT; ++c) {
+        const int64_t id = (d == 0) ? id0 + c : id0;  // n0 % CPT == 0: a thread's cells share a line along d > 0
+#pragma unroll
+        for (int o = 0; o < kVnMaxOfs; ++o) {
+            int64_t sidx = (id - (omin + o)) % nd;
+            if (sidx < 0) sidx += nd;
+            dl[c][o] = (int)((sidx - id) * lay.S[d]);
+        }
+    }
+    int kd = 1, ke = 1;
+    for (int x = 0; x < d; ++x) kd *= KK;
+    for (int x = 0; x < e; ++x) ke *= KK;
+    const int64_t kdL = (int64_t)kd * lay.L, keL = (int64_t)ke * lay.L;
+    const int nd_ = lay.nd, nf_ = lay.K - lay.nd;
+    const float* fb = src.pl + (lp * nf_ - nd_) * lay.L + inner;
+    float* fo = dst.pl + (lp * nf_ - nd_) * lay.L + inner;
+    const int nblk = lay.K / K2;
+    for (int b = 0; b < nblk; ++b) {
+        int q0 = 0, bb = b, kp = 1;
+        for (int x = 0; x < D; ++x) {
+            if (x != d && x != e) {
+                q0 += (bb % KK) * kp;
+                bb /= KK;
+            }
+            kp *= KK;
+        }
+        const int64_t q0L = (int64_t)q0 * lay.L;
+        const bool all_f = (q0 >= nd_);
+        double out[CPT][K2];
+#pragma unroll
+        for (int c = 0; c < CPT; ++c)
+#pragma unroll
+            for (int m = 0; m < K2; ++m) out[c][m] = 0.0;
+#pragma unroll
+        for (int o = 0; o < kVnMaxOfs; ++o) {
+            if (o >= nofs) break;
+            double v[CPT][RS];
+#pragma unroll
+            for (int c = 0; c < CPT; ++c) {
+                if (all_f) {
+                    const float* p = fb + q0L + c + dl[c][o];
+#pragma unroll
+                    for (int le = 0; le < KK; ++le)
+#pragma unroll
+                        for (int ld = 0; ld < KK; ++ld) v[c][le * KK + ld] = (double)p[ld * kdL + le * keL];
+                } else {
+#pragma unroll
+                    for (int le = 0; le < KK; ++le)
+#pragma unroll
+                        for (int ld = 0; ld < KK; ++ld)
+                            v[c][le * KK + ld] = vn_load(lay, src, q0 + ld * kd + le * ke, lp, inner + c + dl[c][o]);
+                }
+                if (RS != K2) v[c][K2] = 0.0;
+            }
+            const double* Mo = sM + o * K2 * RS;
+#pragma unroll
+            for (int l = 0; l < K2; ++l) {  // outer product over l: CPT K2 independent chains
+#pragma unroll
+                for (int m = 0; m < RS; m += 2) {
+                    const double2 mm = *(const double2*)&Mo[l * RS + m];
+#pragma unroll
+                    for (int c = 0; c < CPT; ++c) {
+                        out[c][m] = fma(mm.x, v[c][l], out[c][m]);
+                        if (m + 1 < K2) out[c][m + 1] = fma(mm.y, v[c][l], out[c][m + 1]);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < CPT; ++c) {
+            if (all_f) {
+                float* p = fo + q0L + c;
+#pragma unroll
+                for (int me = 0; me < KK; ++me)
+#pragma unroll
+                    for (int md = 0; md < KK; ++md) p[md * kdL + me * keL] = __double2float_rn(out[c][me * KK + md]);
+            } else {
+#pragma unroll
+                for (int me = 0; me < KK; ++me)
+#pragma unroll
+                    for (int md = 0; md < KK; ++md)
+                        vn_store(lay, dst, q0 + md * kd + me * ke, lp, inner + c, out[c][me * KK + md]);
+            }
+        }
+    }
+}
+
 }  // namespace
 
 int64_t vnode_rec_words(int k) { return vn_rec_words(k); }
@@ -285,6 +416,23 @@ cudaError_t launch_vnode_sweep(const Layout& lay, int d, int e, const double* d_
     if (blocks == 0) return cudaSuccess;
     const int k2 = lay.k * lay.k;
     const size_t smem = (size_t)kVnMaxOfs * k2 * ((k2 + 1) & ~1) * sizeof(double);
+    // CPT = 2 cells per thread where every CTA's 512 cells share their v-cell (SLDG_VN_MULTI=0: off)
+    constexpr int CPT = 2;
+    const char* em = getenv("SLDG_VN_MULTI");
+    const bool multi = !(em && atoi(em) == 0) && lay.k <= 3 && d != lay.D - 1 && lay.n[0] % CPT == 0 &&
+                       (int64_t)lay.K * lay.L < ((int64_t)1 << 31) &&
+                       ((e == lay.D - 1) ? lay.L : lay.S[e]) % (256 * CPT) == 0;
+    if (multi) {
+        const unsigned mb = (unsigned)(lay.cells / (256 * CPT));
+        switch (lay.k) {
+            case 1: vnode_sweep_multi<1, CPT><<<mb, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
+            case 2: vnode_sweep_multi<2, CPT><<<mb, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
+            case 3: vnode_sweep_multi<3, CPT><<<mb, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
+            case 4: vnode_sweep_multi<4, CPT><<<mb, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
+            default: return cudaErrorInvalidValue;
+        }
+        return cudaGetLastError();
+    }
     switch (lay.k) {
         case 1: vnode_sweep_kernel<1><<<blocks, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;
         case 2: vnode_sweep_kernel<2><<<blocks, 256, smem, s>>>(lay, d, e, d_rec, src, dst); break;

@@ -62,6 +62,44 @@ def test_vnodes_parity(dims, k, dim, vdim, precision):
     g.destroy()
 
 
+# shapes where every CTA's 512 cells share their v-cell: the CPT = 2 kernel (vnode_sweep_multi)
+MULTI_CASES = [
+    ([64, 8, 16], 3, 0, 2),       # x1 (d = 0) with v = the layer dim
+    ([32, 16, 8, 4], 3, 1, 2),    # x2 with v1 (S_e = 512)
+    ([512, 6], 3, 0, 1),          # 2D C3-shaped
+    ([64, 16, 4, 5], 2, 0, 2),    # 4D k = 2
+    ([128, 4, 8], 1, 0, 2),       # k = 1
+]
+
+
+@pytest.mark.parametrize("precision", ["mixed", "fp64"])
+@pytest.mark.parametrize("dims,k,dim,vdim", MULTI_CASES)
+def test_vnodes_multi_cell_kernel(dims, k, dim, vdim, precision, monkeypatch):
+    """Two cells per thread (vnode_sweep_multi): the same operation order per output as the
+    one-cell kernel, so bit-identical to it (SLDG_VN_MULTI=0), and within the parity bar of the
+    oracle; shifts of several cells of both signs with 2- and 3-offset v-cells."""
+    from paper_1603_07008_b200 import Grid
+    D, K = len(dims), k ** len(dims)
+    nd = 1 if precision == "mixed" else K
+    c = sldg_inputs.random_coeffs(dims, k, 33)
+    src = oracle.round_layout(c, K, nd)
+    g = Grid(dims, k, precision=precision)
+    nv = dims[vdim]
+    # a v-cell spans 0.4 and 2.0 cells of shift (2- and 3-offset cells, within kVnMaxOfs)
+    for width in [0.4, 2.0]:
+        nodal = vnodes.nodal_velocity_field(nv, -3.0, 3.0, k, width * nv / 6.0)
+        outs = []
+        for multi in ["1", "0"]:
+            monkeypatch.setenv("SLDG_VN_MULTI", multi)
+            g.set_coeffs(c)
+            g.advect_vnodes(dim, vdim, nodal)
+            outs.append(g.get_coeffs())
+        assert outs[0].tobytes() == outs[1].tobytes(), f"multi-cell kernel differs: dims={dims} width={width}"
+        ref = vnodes.advect_vnodes(src, dims, k, dim, vdim, nodal, n_double=nd)
+        _parity(outs[0], ref, K, precision, src, f"multi dims={dims} dim={dim} vdim={vdim} width={width}")
+    g.destroy()
+
+
 def test_vnodes_mass_and_bad_field():
     from paper_1603_07008_b200 import Grid, SldgError
     dims, k = [32, 16], 3
