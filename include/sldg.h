@@ -91,22 +91,12 @@ typedef struct {
     int max_halo;               /* halo layers allocated per side; <= 0 selects 2          */
     int flags;                  /* SLDG_DIST_* bits                                        */
 } sldg_dist;
-/* Run sweeps along the sharded dim through the halo path even when world == 1 (the ring
- * neighbour is the rank itself: halo layers are device copies).  Exercises the exact halo
- * addressing of multi-GPU runs on one GPU; no NCCL communicator is needed. */
-#define SLDG_DIST_FORCE_HALO 1
-/* Every sweep along the layer dim takes the transpose path (testing on one GPU; see
- * sldg_transpose_plan).  Implies the halo layout. */
-#define SLDG_DIST_FORCE_TRANSPOSE 2
-/* world == 1 only: create a one-rank NCCL communicator and send this rank's own halo layers,
- * transpose blocks and density partials through ncclSend/ncclRecv/ncclAllGather instead of
- * device copies -- the multi-GPU NCCL code paths (message pointers, counts, pairing order)
- * exercised on one GPU. */
-#define SLDG_DIST_NCCL_SELF 4
+/* Test-only bits of `flags` (one-GPU stand-ins for the multi-GPU paths) are in
+ * include/sldg_testing.h. */
 /* Peer-mapped halos: the pad layers of both coefficient arrays are CUDA
  * virtual-memory mappings of the ring neighbours' edge layers (left pad = the left neighbour's
  * last `max_halo` layers, right pad = the right neighbour's first ones; with world == 1 and
- * SLDG_DIST_FORCE_HALO, this rank's own).  A sweep along the sharded dim whose halo fits the
+ * SLDG_DIST_FORCE_HALO (sldg_testing.h), this rank's own).  A sweep along the sharded dim whose halo fits the
  * pads is then ONE launch over all local layers whose boundary tiles read the neighbours' HBM
  * directly (NVLink for another GPU): no exchange step.  world > 1: an NCCL fence with both
  * neighbours before and after such a sweep (device-side, capturable); the chunks are shared
@@ -114,10 +104,6 @@ typedef struct {
  * with ENOTSUP unless sldg_peer_halo_check accepts the layout at the device's allocation
  * granularity. */
 #define SLDG_DIST_PEER_HALO 8
-/* Testing (with SLDG_DIST_PEER_HALO, world == 1): the rank's own edge chunks are exported as
- * POSIX file descriptors, fetched back with pidfd_getfd and imported -- the descriptor path of
- * world > 1 exercised in one process. */
-#define SLDG_DIST_PEER_VIA_FD 16
 
 /* Create a grid (zero-filled).  k in 1..SLDG_MAX_K coefficients per dim (the paper's order
  * o = p+1).  dist may be NULL (single GPU).  The device is the caller's current

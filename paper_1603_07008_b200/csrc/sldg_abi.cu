@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "sldg_internal.h"
+#include "../../include/sldg_testing.h"
 
 using namespace sldg;
 
