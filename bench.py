@@ -532,6 +532,21 @@ def main():
             traffic_all = {str(d): nd.get(f"{args.config}_{args.precision}_k{k}_dim{d}") for d in sweep_dims}
         except Exception:
             traffic_all = None
+        # secondary roofline: fp64-pipe and XU (F2F) activity of the dominant kernel
+        # from the ncu launch list of this config (profiles/ncu_pipe.json)
+        secondary = {"bound": "fp64 pipe", "dfma_per_cell_per_sweep": 2 * k * K,
+                     "fp64_pipe_pct": None, "xu_pct": None,
+                     "source": "profiles/ncu_pipe.json: sm__pipe_fp64_cycles_active / sm__inst_executed_pipe_xu "
+                               "(% of peak sustained active) of the launch-list pass of this config"}
+        try:
+            with open(os.path.join(ROOT, "profiles", "ncu_pipe.json")) as f:
+                npj = json.load(f)
+            key = f"{args.config}_{args.precision}_k{k}_dim{dom}" if dom >= 0 else f"{args.config}_{args.precision}_k{k}_fused01"
+            if key in npj:
+                secondary["fp64_pipe_pct"] = npj[key]["fp64_pipe_pct"]
+                secondary["xu_pct"] = npj[key]["xu_pct"]
+        except Exception:
+            pass
         cpu = None
         if not args.no_cpu_baseline and world == 1:
             cpu = oracle_baseline(dims, kinds, k, args.precision, args.cpu_lines, eps=args.eps)
@@ -558,6 +573,7 @@ def main():
                                            "graph-replayed timed region") if use_graph else
                                           "CUDA events around each sweep launch inside the timed region",
                          "avg_launch_ms": d_ms / d_n if d_n else None,
+                         "secondary": secondary,
                          "kernels": {kn: {"dims": e["dims"], "launches_per_step": e["launches"] / max(1, launch_steps),
                                           "ms_per_launch": e["ms"] / max(1, e["launches"]),
                                           "achieved_gbs": e["bytes"] / (e["ms"] * 1e-3) / 1e9 if e["ms"] else None,

@@ -24,7 +24,7 @@ def short(name):
     return n.replace("void ", "").replace("sldg::", "")
 
 
-def launches(path, out, dram_json=None, key=None):
+def launches(path, out, dram_json=None, key=None, pipe_json=None):
     rows = list(csv.reader(open(path)))
     start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
     hdr = rows[start]
@@ -42,6 +42,10 @@ def launches(path, out, dram_json=None, key=None):
         elif m.startswith("dram__bytes"):
             scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
             d["read" if "read" in m else "write"] = val * scale
+        elif m == "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active":
+            d["fp64"] = val
+        elif m == "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active":
+            d["xu"] = val
     tot = sum(d.get("ms", 0) for d in per.values())
     fam = defaultdict(float)
     for d in per.values():
@@ -75,6 +79,12 @@ def launches(path, out, dram_json=None, key=None):
         for nm, d in zip(names, first):
             db[f"{base}_{nm}"] = d.get("read", 0) + d.get("write", 0)
         json.dump(db, open(dram_json, "w"), indent=1, sort_keys=True)
+        if pipe_json:  # secondary roofline: fp64-pipe and XU activity per sweep
+            pb = json.load(open(pipe_json)) if os.path.exists(pipe_json) else {}
+            for nm, d in zip(names, first):
+                if "fp64" in d:
+                    pb[f"{base}_{nm}"] = {"fp64_pipe_pct": d["fp64"], "xu_pct": d.get("xu")}
+            json.dump(pb, open(pipe_json, "w"), indent=1, sort_keys=True)
     print(out)
 
 
@@ -118,6 +128,7 @@ if __name__ == "__main__":
     if sys.argv[1] == "launches":
         dj = sys.argv[sys.argv.index("--dram-json") + 1] if "--dram-json" in sys.argv else None
         key = sys.argv[sys.argv.index("--key") + 1] if "--key" in sys.argv else None
-        launches(sys.argv[2], sys.argv[3], dj, key)
+        pj = sys.argv[sys.argv.index("--pipe-json") + 1] if "--pipe-json" in sys.argv else None
+        launches(sys.argv[2], sys.argv[3], dj, key, pj)
     else:
         full(sys.argv[2], sys.argv[3])
