@@ -18,6 +18,7 @@ core) on a bounded sample of the same workload (sampled lines of every sweep).
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -69,15 +70,26 @@ def load_peak():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms.  Started before the warm-up
+    steps (nvidia-smi's start-up, NVML init included, then overlaps them, not the timed region);
+    summary() keeps only the samples taken between mark(True) and mark(False) -- the timed
+    region -- when there are any."""
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.t_begin = None
+        self.t_end = None
+
+    def mark(self, begin: bool):  # wall-clock marks, compared with nvidia-smi's own sample timestamps
+        if begin:
+            self.t_begin = datetime.datetime.now()
+        else:
+            self.t_end = datetime.datetime.now()
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
@@ -106,10 +118,22 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons, masks = [], None, set(), set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        rows = []
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
+            if len(parts) < 8:
                 continue
+            try:
+                ts = datetime.datetime.strptime(parts[0], "%Y/%m/%d %H:%M:%S.%f")
+            except ValueError:
+                ts = None
+            rows.append((ts, parts[1:]))
+        if self.t_begin is not None:
+            t1 = self.t_end or datetime.datetime.max
+            inside = [r for r in rows if r[0] is not None and self.t_begin <= r[0] <= t1]
+            if inside:
+                rows = inside
+        for _, parts in rows:
             try:
                 sm.append(float(parts[0]))
                 mx = float(parts[1])
@@ -297,6 +321,9 @@ def main():
                     help="also time the all-fp64 layout on a slab of the workload (mixed_vs_fp64)")
     ap.add_argument("--vlasov", action=argparse.BooleanOptionalAction, default=True,
                     help="also time the Vlasov-Poisson Strang step (NEXT-2) on the same grid")
+    ap.add_argument("--kernel-events", action=argparse.BooleanOptionalAction, default=True,
+                    help="diagnostic: --no-kernel-events times the step without the per-launch CUDA events "
+                         "(no roofline.achieved)")
     ap.add_argument("--graph", action=argparse.BooleanOptionalAction, default=True,
                     help="replay the timed steps from a CUDA graph of one split step (1 GPU)")
     ap.add_argument("--sweeps", default=None, help="comma list of dims to run (default: all)")
@@ -389,6 +416,7 @@ def main():
         torch.cuda.synchronize()
         g.sync()
 
+    clk = ClockSampler(local_rank).__enter__()  # nvidia-smi starts during the warm-up
     mass0 = g.mass()
     for _ in range(args.warmup):
         step()
@@ -423,24 +451,26 @@ def main():
     # ---------------------------------------------------------------- device-timed region
     if not use_graph:
         g.kernel_time(reset=True)
-        g.profile(True)
+        g.profile(args.kernel_events)
     launches0 = g.launch_count()
     # one event between consecutive steps (same stream, no host sync): per-step times for the
     # median of the K repetitions (SURVEY 8(d) "median of >= 5 repetitions")
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0, e1 = evs[0], evs[-1]
-    with ClockSampler(local_rank) as clk:
-        barrier()
+    barrier()
+    clk.mark(True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+    for i in range(args.steps):
+        if graph is not None:
+            graph.launch()
+        else:
+            step()
         with torch.cuda.stream(stream):
-            e0.record(stream)
-        for i in range(args.steps):
-            if graph is not None:
-                graph.launch()
-            else:
-                step()
-            with torch.cuda.stream(stream):
-                evs[i + 1].record(stream)
-        barrier()
+            evs[i + 1].record(stream)
+    barrier()
+    clk.mark(False)
+    clk.__exit__(None, None, None)
     ms = e0.elapsed_time(e1)
     step_times = torch.tensor([evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)], dtype=torch.float64,
                               device="cuda")
