@@ -511,7 +511,9 @@ def main():
             pt.numpy()[:] = f
             pinned.append(pt)
         h2d = sum(p.numel() * 8 for p in pinned)
+        eclk = ClockSampler(local_rank).__enter__()
         barrier()
+        eclk.mark(True)
         t0 = time.perf_counter()
         for _ in range(args.steps):
             first = 0
@@ -523,13 +525,16 @@ def main():
             g.mass()  # D2H read of the step's diagnostic (blocking)
         barrier()
         e2e_s = time.perf_counter() - t0
+        eclk.mark(False)
+        eclk.__exit__(None, None, None)
         te = torch.tensor([e2e_s], dtype=torch.float64, device="cuda")
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_s = float(te.item())
         e2e = {"value": len(sweeps) * cells * K * args.steps / e2e_s / 1e9, "unit": "GDoF/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": 8 * world,
-               "api": "sldg_advect (host pinned CFL fields, one per sweep) + sldg_mass (D2H) per step"}
+               "api": "sldg_advect (host pinned CFL fields, one per sweep) + sldg_mass (D2H) per step",
+               "clocks": eclk.summary()}
 
     launch_steps = 2 if use_graph else args.steps  # steps the per-kernel events cover
     if rank == 0:
