@@ -25,7 +25,9 @@
 // offsets: pad * u and layers * u are multiples of it for both sections' per-layer bytes u, on
 // every rank (peer_halo_check).  Cross-process mapping (world > 1) exports each chunk as a POSIX
 // file descriptor; the descriptors are fetched with pidfd_getfd(2) after an NCCL all-gather of
-// (pid, fd) -- this part needs two GPUs and is not exercised by the one-GPU tests.
+// (pid, fd).  SLDG_DIST_PEER_VIA_FD runs the export / pidfd_getfd / import / map route in one
+// process (world == 1, tested); the all-gather, the fences and NVLink reads need two GPUs
+// (tests/test_gpu_multi.py, skipped on one-GPU boxes).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
