@@ -100,7 +100,8 @@ typedef struct {
  * pads is then ONE launch over all local layers whose boundary tiles read the neighbours' HBM
  * directly (NVLink for another GPU): no exchange step.  world > 1: an NCCL fence with both
  * neighbours before and after such a sweep (device-side, capturable); the chunks are shared
- * between processes as POSIX file descriptors (pidfd_getfd).  Creation is collective and fails
+ * between processes as POSIX file descriptors over abstract unix sockets (SCM_RIGHTS; no ptrace
+ * rights needed).  Creation is collective and fails
  * with ENOTSUP unless sldg_peer_halo_check accepts the layout at the device's allocation
  * granularity. */
 #define SLDG_DIST_PEER_HALO 8

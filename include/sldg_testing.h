@@ -20,7 +20,7 @@
  * exercised on one GPU. */
 #define SLDG_DIST_NCCL_SELF 4
 /* Testing (with SLDG_DIST_PEER_HALO, world == 1): the rank's own edge chunks are exported as
- * POSIX file descriptors, fetched back with pidfd_getfd and imported -- the descriptor path of
+ * POSIX file descriptors, passed back over the rank's own unix socket and imported -- the descriptor path of
  * world > 1 exercised in one process. */
 #define SLDG_DIST_PEER_VIA_FD 16
 

@@ -24,18 +24,24 @@
 // Physical chunks must be multiples of the allocation granularity at granularity-aligned
 // offsets: pad * u and layers * u are multiples of it for both sections' per-layer bytes u, on
 // every rank (peer_halo_check).  Cross-process mapping (world > 1) exports each chunk as a POSIX
-// file descriptor; the descriptors are fetched with pidfd_getfd(2) after an NCCL all-gather of
-// (pid, fd).  SLDG_DIST_PEER_VIA_FD runs the export / pidfd_getfd / import / map route in one
-// process (world == 1, tested); the all-gather, the fences and NVLink reads need two GPUs
-// (tests/test_gpu_multi.py, skipped on one-GPU boxes).
+// file descriptor and hands them to the two ring neighbours over an abstract-namespace unix socket
+// (SCM_RIGHTS; the socket names go round in an NCCL all-gather) -- no ptrace rights needed.
+// SLDG_DIST_PEER_VIA_FD runs the export / socket / import / map route in one process (world == 1,
+// tested); the all-gather, the fences and NVLink reads need two GPUs (tests/test_gpu_multi.py,
+// skipped on one-GPU boxes).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
-#include <sys/prctl.h>
-#include <sys/syscall.h>
+#include <poll.h>
+#include <stddef.h>
+#include <string.h>
+#include <sys/socket.h>
+#include <sys/un.h>
 #include <unistd.h>
 
+#include <atomic>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sldg_internal.h"
@@ -104,6 +110,82 @@ void section_units(const Layout& L, size_t* u64, size_t* u32)
     *u32 = (size_t)L.L * 4 * (size_t)(L.K - L.nd);
 }
 
+
+// ---- descriptor passing over abstract unix sockets (SCM_RIGHTS) ------------------------------
+constexpr int kFdSlots = 8;  // [b][s][low / high] edge chunks of one rank
+
+std::string sock_name(long long pid, long long seq) { return "sldg-peer-" + std::to_string(pid) + "-" + std::to_string(seq); }
+
+socklen_t sock_addr(const std::string& name, sockaddr_un* a)
+{
+    memset(a, 0, sizeof(*a));
+    a->sun_family = AF_UNIX;
+    memcpy(a->sun_path + 1, name.data(), name.size());  // sun_path[0] = 0: abstract namespace
+    return (socklen_t)(offsetof(sockaddr_un, sun_path) + 1 + name.size());
+}
+
+bool send_fds(int sock, const int* fds)
+{
+    char present[kFdSlots];
+    int valid[kFdSlots], nv = 0;
+    for (int i = 0; i < kFdSlots; ++i) {
+        present[i] = fds[i] >= 0;
+        if (fds[i] >= 0) valid[nv++] = fds[i];
+    }
+    iovec iov = {present, sizeof(present)};
+    msghdr msg = {};
+    msg.msg_iov = &iov;
+    msg.msg_iovlen = 1;
+    alignas(cmsghdr) char cbuf[CMSG_SPACE(sizeof(int) * kFdSlots)] = {};
+    if (nv) {
+        msg.msg_control = cbuf;
+        msg.msg_controllen = CMSG_SPACE(sizeof(int) * nv);
+        cmsghdr* c = CMSG_FIRSTHDR(&msg);
+        c->cmsg_level = SOL_SOCKET;
+        c->cmsg_type = SCM_RIGHTS;
+        c->cmsg_len = CMSG_LEN(sizeof(int) * nv);
+        memcpy(CMSG_DATA(c), valid, sizeof(int) * nv);
+    }
+    return sendmsg(sock, &msg, MSG_NOSIGNAL) == (ssize_t)sizeof(present);
+}
+
+bool recv_fds(int sock, int* fds)
+{
+    char present[kFdSlots];
+    iovec iov = {present, sizeof(present)};
+    msghdr msg = {};
+    msg.msg_iov = &iov;
+    msg.msg_iovlen = 1;
+    alignas(cmsghdr) char cbuf[CMSG_SPACE(sizeof(int) * kFdSlots)] = {};
+    msg.msg_control = cbuf;
+    msg.msg_controllen = sizeof(cbuf);
+    for (int i = 0; i < kFdSlots; ++i) fds[i] = -1;
+    if (recvmsg(sock, &msg, MSG_CMSG_CLOEXEC) != (ssize_t)sizeof(present)) return false;
+    int got[kFdSlots], ng = 0;
+    for (cmsghdr* c = CMSG_FIRSTHDR(&msg); c; c = CMSG_NXTHDR(&msg, c))
+        if (c->cmsg_level == SOL_SOCKET && c->cmsg_type == SCM_RIGHTS) {
+            ng = (int)((c->cmsg_len - CMSG_LEN(0)) / sizeof(int));
+            memcpy(got, CMSG_DATA(c), sizeof(int) * ng);
+        }
+    for (int i = 0, j = 0; i < kFdSlots; ++i)
+        if (present[i]) fds[i] = (j < ng) ? got[j++] : -1;
+    return true;
+}
+
+// serves this rank's descriptors to the two neighbour connections (or stops when the listening
+// socket is shut down, or after 60 s without a connection)
+void serve_fds(int lsock, const int* fds)
+{
+    for (int served = 0; served < 2;) {
+        pollfd p = {lsock, POLLIN, 0};
+        if (poll(&p, 1, 60000) <= 0 || !(p.revents & POLLIN)) return;
+        const int c = accept4(lsock, nullptr, nullptr, SOCK_CLOEXEC);
+        if (c < 0) return;
+        send_fds(c, fds);
+        close(c);
+        ++served;
+    }
+}
 }  // namespace
 
 std::string peer_halo_check(const Layout& L, int world, size_t gran)
@@ -180,7 +262,7 @@ void peer_free(sldg_grid g)
 // world > 1 this is collective: a rank that fails locally still takes part in the all-gather
 // and the closing all-reduce (carrying its failure), so every rank returns the error together.
 // via_fd (world == 1, testing): the rank's own chunks go through the descriptor export /
-// pidfd_getfd / import path of world > 1.
+// unix-socket / import path of world > 1.
 std::string peer_alloc(sldg_grid g, bool via_fd)
 {
     const Layout& L = g->lay;
@@ -250,12 +332,16 @@ std::string peer_alloc(sldg_grid g, bool via_fd)
                 nb[b][s][1] = P->edge[b][s][0];
             }
     } else {
-        // export my 8 edge chunks, all-gather (pid, fds) -- pid -1 marks a failed rank -- and
-        // fetch the neighbours' descriptors
-        constexpr int kW = 9;  // pid + [b][s][lo/hi] fds
-        std::vector<long long> mine(kW, -1), all((size_t)kW * g->world, -1);
+        // export my 8 edge chunks as descriptors, listen on an abstract socket, all-gather its
+        // name (pid, sequence number; pid -1 marks a failed rank), then fetch the neighbours'
+        // descriptors from their sockets while a thread serves mine
+        constexpr int kW = 2;
+        static std::atomic<long long> seq_ctr{0};
+        const long long seq = seq_ctr++;
+        int my_fds[kFdSlots];
+        for (int i = 0; i < kFdSlots; ++i) my_fds[i] = -1;
+        int lsock = -1;
         if (err.empty()) {
-            prctl(PR_SET_PTRACER, PR_SET_PTRACER_ANY, 0, 0, 0);  // let the peers' pidfd_getfd reach our fds
             for (int b = 0; b < 2; ++b)
                 for (int s = 0; s < 2; ++s)
                     for (int e = 0; e < 2 && err.empty(); ++e) {
@@ -265,10 +351,20 @@ std::string peer_alloc(sldg_grid g, bool via_fd)
                                                            CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR, 0) != CUDA_SUCCESS)
                             err = "cuMemExportToShareableHandle failed";
                         else
-                            mine[1 + (b * 2 + s) * 2 + e] = fd;
+                            my_fds[(b * 2 + s) * 2 + e] = fd;
                     }
         }
-        mine[0] = err.empty() ? (long long)getpid() : -1;
+        if (err.empty()) {
+            sockaddr_un a;
+            const socklen_t len = sock_addr(sock_name(getpid(), seq), &a);
+            lsock = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+            if (lsock < 0 || bind(lsock, (sockaddr*)&a, len) != 0 || listen(lsock, 4) != 0)
+                err = "cannot listen on the descriptor-exchange socket";
+        }
+        std::thread server;
+        if (err.empty()) server = std::thread(serve_fds, lsock, my_fds);
+        std::vector<long long> mine = {err.empty() ? (long long)getpid() : -1, seq};
+        std::vector<long long> all((size_t)kW * g->world, -1);
         long long* dbuf = nullptr;
         bool comm_ok = true;
         if (multi) {
@@ -286,31 +382,36 @@ std::string peer_alloc(sldg_grid g, bool via_fd)
         for (int r = 0; r < g->world && comm_ok; ++r) any_failed |= all[(size_t)r * kW] < 0;
         const int left = (g->rank + g->world - 1) % g->world, right = (g->rank + 1) % g->world;
         std::vector<int> fetched;
-        auto import = [&](int peer, int b, int s, int e, CUmemGenericAllocationHandle* h) -> bool {
-            const long long* row = &all[(size_t)peer * kW];
-            int pfd = (int)syscall(SYS_pidfd_open, (pid_t)row[0], 0);
-            if (pfd < 0) return false;
-            int fd = (int)syscall(SYS_pidfd_getfd, pfd, (int)row[1 + (b * 2 + s) * 2 + e], 0);
-            close(pfd);
-            if (fd < 0) return false;
-            fetched.push_back(fd);
-            if (d.cuMemImportFromShareableHandle(h, (void*)(uintptr_t)fd, CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) !=
-                CUDA_SUCCESS)
+        auto fetch = [&](int peer, int* fds) -> bool {  // the peer's 8 descriptors
+            sockaddr_un a;
+            const socklen_t len = sock_addr(sock_name(all[(size_t)peer * kW], all[(size_t)peer * kW + 1]), &a);
+            const int c = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
+            if (c < 0) return false;
+            const bool ok = connect(c, (sockaddr*)&a, len) == 0 && recv_fds(c, fds);
+            close(c);
+            for (int i = 0; i < kFdSlots; ++i)
+                if (fds[i] >= 0) fetched.push_back(fds[i]);
+            return ok;
+        };
+        auto import = [&](int fd, CUmemGenericAllocationHandle* h) -> bool {
+            if (fd < 0 || d.cuMemImportFromShareableHandle(h, (void*)(uintptr_t)fd,
+                                                           CU_MEM_HANDLE_TYPE_POSIX_FILE_DESCRIPTOR) != CUDA_SUCCESS)
                 return false;
             P->handles.push_back(*h);
             return true;
         };
-        bool ok = !any_failed;
+        bool ok = !any_failed && err.empty();
+        int lf[kFdSlots], rf[kFdSlots];
+        if (ok) ok = fetch(left, lf) && fetch(right, rf);
         for (int b = 0; b < 2 && ok; ++b)
             for (int s = 0; s < 2 && ok; ++s) {
                 if (!u[s]) continue;
-                ok = import(left, b, s, 1, &nb[b][s][0]) && import(right, b, s, 0, &nb[b][s][1]);
+                ok = import(lf[(b * 2 + s) * 2 + 1], &nb[b][s][0]) && import(rf[(b * 2 + s) * 2 + 0], &nb[b][s][1]);
             }
         if (err.empty() && !ok)
             err = any_failed ? "another rank failed to set up its peer-mapped halo chunks"
-                             : "importing a neighbour's chunk failed (pidfd_getfd / cuMemImportFromShareableHandle)";
-        // nobody closes its exported descriptors before every rank has fetched them; the sum
-        // of failures decides for all
+                             : "fetching or importing a neighbour's chunk failed (unix socket / cuMemImportFromShareableHandle)";
+        // the sum of failures decides for all; a server whose neighbours gave up stops here
         if (multi && comm_ok) {
             int* flag = (int*)dbuf;
             const int mine_bad = err.empty() ? 0 : 1;
@@ -322,9 +423,12 @@ std::string peer_alloc(sldg_grid g, bool via_fd)
             if (err.empty() && (!comm_ok || bad)) err = "another rank failed to map its peer-mapped halo chunks";
         }
         if (multi && !comm_ok && err.empty()) err = "the chunk descriptor exchange failed";
+        if (lsock >= 0) shutdown(lsock, SHUT_RDWR);  // wakes a server still waiting (failure paths)
+        if (server.joinable()) server.join();
+        if (lsock >= 0) close(lsock);
         for (int fd : fetched) close(fd);
-        for (int i = 1; i < kW; ++i)
-            if (mine[i] >= 0) close((int)mine[i]);
+        for (int i = 0; i < kFdSlots; ++i)
+            if (my_fds[i] >= 0) close(my_fds[i]);
         if (dbuf) cudaFree(dbuf);
         if (!err.empty()) return err;
         if (multi) {

@@ -126,7 +126,7 @@ def test_peer_halo_mass_conserved():
 
 def test_peer_halo_descriptor_path_in_one_process():
     """SLDG_DIST_PEER_VIA_FD: the edge chunks go through the multi-process route (export as POSIX
-    file descriptors, pidfd_getfd, import, map) with the rank as its own neighbour; the sweeps
+    file descriptors, passed over a unix socket (SCM_RIGHTS), import, map) with the rank as its own neighbour; the sweeps
     are bit-identical to the directly mapped pads."""
     dims, k, pad = [32, 32, 32, 32], 3, 8
     ga = _Grid(dims, k, precision="mixed", force_halo=True, peer_halo=True, max_halo=pad)
