@@ -857,3 +857,26 @@ def test_windowed_d0_matches_oracle(dims, k, precision):
             assert got.tobytes() == ref.tobytes()  # integer shift: an exact rotation
         assert_parity(got, ref, K, precision, f"dims={dims} k={k} nu={shift} mask={mask}", ref_in, 0, k)
     g.destroy()
+
+
+@pytest.mark.parametrize("precision", ["fp64", "mixed"])
+def test_windowed_d0_per_line_fields_and_halo_layout(precision):
+    """sweep_d0_win on a 3D grid: per-line fields over dims 1 and 2 (the producer derives each
+    line's field entry from its line and layer index), and the same sweeps on a grid with the
+    halo layout (pad layers shift every layer's address) -- both against the oracle."""
+    dims, k = ([4096, 3, 4], 4) if precision == "fp64" else ([4096, 2, 3], 7)
+    D, K = len(dims), k ** len(dims)
+    c = sldg_inputs.random_coeffs(dims, k, 2718)
+    ref_in = oracle_input(c, K, precision)
+    rng = np.random.default_rng(5)
+    for kw in [{}, {"force_halo": True, "max_halo": 2}]:
+        g = _Grid(dims, k, precision=precision, **kw)
+        assert g.sweep_kernel(0) == "sweep_d0_win", g.sweep_kernel(0)
+        for mask in [2, 4, 6]:
+            nf = int(np.prod([dims[e] for e in range(D) if mask >> e & 1]))
+            field = rng.uniform(-1.5 * dims[0], 1.5 * dims[0], nf)
+            g.set_coeffs(c)
+            g.advect(0, field=field, field_mask=mask)
+            ref = oracle.advect(ref_in, dims, k, 0, field=field, field_mask=mask, n_double=n_double(precision, K))
+            assert_parity(g.get_coeffs(), ref, K, precision, f"win dims={dims} mask={mask} {kw}", ref_in, 0, k)
+        g.destroy()
