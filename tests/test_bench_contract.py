@@ -53,3 +53,24 @@ def test_oracle_baseline_all_cores_is_bit_identical():
     assert res["bit_identical_all_vs_1"] is True
     assert res["nproc"] >= 1 and res["cores_all"] == res["nproc"] and res["cpu_model"]
     assert res["value"] > 0 and res["value_all_cores"] > 0
+
+
+def test_clock_sampler_keeps_the_timed_region():
+    """The clocks line is taken from nvidia-smi samples timestamped inside the timed region
+    (the sampler starts before the warm-up); with none inside, every sample is used."""
+    import datetime
+    sys.path.insert(0, ROOT)
+    import bench
+    c = bench.ClockSampler(0)
+    now = datetime.datetime.now()
+
+    def line(dt_s, mhz, cap):
+        t = (now + datetime.timedelta(seconds=dt_s)).strftime("%Y/%m/%d %H:%M:%S.%f")[:-3]
+        return f"{t}, {mhz}, 1965, 0x4, Not Active, Not Active, Not Active, {'Active' if cap else 'Not Active'}"
+
+    c.lines = [line(-1.0, 1965, False), line(0.1, 1700, True), line(0.3, 1690, True), line(2.0, 1965, False)]
+    c.t_begin, c.t_end = now, now + datetime.timedelta(seconds=0.5)
+    s = c.summary()
+    assert s["samples"] == 2 and s["sm_mhz"] == 1695.0 and s["reasons"] == ["sw_power_cap"]
+    c.t_begin, c.t_end = now + datetime.timedelta(seconds=0.6), now + datetime.timedelta(seconds=0.7)
+    assert c.summary()["samples"] == 4  # nothing inside: all samples
