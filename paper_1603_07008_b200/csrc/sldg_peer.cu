@@ -181,9 +181,13 @@ void serve_fds(int lsock, const int* fds)
         if (poll(&p, 1, 60000) <= 0 || !(p.revents & POLLIN)) return;
         const int c = accept4(lsock, nullptr, nullptr, SOCK_CLOEXEC);
         if (c < 0) return;
-        send_fds(c, fds);
+        ucred cr = {};
+        socklen_t crl = sizeof(cr);
+        if (getsockopt(c, SOL_SOCKET, SO_PEERCRED, &cr, &crl) == 0 && cr.uid == getuid()) {  // same user only
+            send_fds(c, fds);
+            ++served;
+        }
         close(c);
-        ++served;
     }
 }
 }  // namespace
@@ -387,7 +391,12 @@ std::string peer_alloc(sldg_grid g, bool via_fd)
             const socklen_t len = sock_addr(sock_name(all[(size_t)peer * kW], all[(size_t)peer * kW + 1]), &a);
             const int c = socket(AF_UNIX, SOCK_STREAM | SOCK_CLOEXEC, 0);
             if (c < 0) return false;
-            const bool ok = connect(c, (sockaddr*)&a, len) == 0 && recv_fds(c, fds);
+            // the listener must be the process the all-gather named (SO_PEERCRED), not a squatter
+            ucred cr = {};
+            socklen_t crl = sizeof(cr);
+            const bool ok = connect(c, (sockaddr*)&a, len) == 0 &&
+                            getsockopt(c, SOL_SOCKET, SO_PEERCRED, &cr, &crl) == 0 &&
+                            (long long)cr.pid == all[(size_t)peer * kW] && cr.uid == getuid() && recv_fds(c, fds);
             close(c);
             for (int i = 0; i < kFdSlots; ++i)
                 if (fds[i] >= 0) fetched.push_back(fds[i]);
